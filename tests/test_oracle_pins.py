@@ -1,0 +1,253 @@
+"""Pins of the CPU oracle against things other than itself (no GPU).
+
+Each test names the PAPER.md passage whose mathematics fixes the expected
+value: closed forms, finite differences, invariants, brute force and the
+independent exact LP (network simplex).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import pins_oracle as po
+from oracle.exact_lp import brute_force_assignment, solve_exact
+
+E1 = math.exp(-1.0)
+
+
+# ---------------------------------------------------------------- Eq. (7)-(9)
+def test_plan_closed_form():
+    # Eq. (7) with f=g=0, C^k=0, eta=1: every entry exp(-1)
+    X = po.plan(np.zeros(2), np.zeros(3), np.zeros((2, 3)), 1.0)
+    assert np.allclose(X, E1, rtol=0, atol=1e-16)
+
+
+def test_dual_objective_and_gradient_closed_form():
+    # Eq. (8): P = 0 + 0 - 1 * 4 e^-1 ; Eq. (9): grad_f = 0.5 - 2 e^-1
+    a = b = np.array([0.5, 0.5])
+    P = po.dual_objective(np.zeros(2), np.zeros(2), np.zeros((2, 2)), a, b, 1.0)
+    assert abs(P - (-4 * E1)) < 1e-15
+    gf, gg = po.dual_gradient(np.zeros(2), np.zeros(2), np.zeros((2, 2)), a, b, 1.0)
+    assert np.allclose(gf, 0.5 - 2 * E1, atol=1e-15) and np.allclose(gg, 0.5 - 2 * E1, atol=1e-15)
+
+
+def test_gauge_invariance():
+    # (f + c e, g - c e) leaves X~ unchanged and P unchanged when sum a = sum b = 1
+    rng = np.random.default_rng(5)
+    C = rng.random((4, 3)); a = np.full(4, .25); b = np.full(3, 1 / 3)
+    f, g = rng.normal(size=4), rng.normal(size=3)
+    X1 = po.plan(f, g, C, 0.3); X2 = po.plan(f + 0.7, g - 0.7, C, 0.3)
+    assert np.allclose(X1, X2, rtol=1e-13)
+    assert abs(po.dual_objective(f, g, C, a, b, .3) - po.dual_objective(f + .7, g - .7, C, a, b, .3)) < 1e-13
+
+
+@pytest.mark.parametrize("eta", [1.0, 0.1])
+def test_gradient_matches_finite_differences(eta):
+    rng = np.random.default_rng(11)
+    for _ in range(10):
+        m, n = rng.integers(2, 7), rng.integers(2, 6)
+        C = rng.random((m, n)); a = po_norm(rng.random(m) + .1); b = po_norm(rng.random(n) + .1)
+        f, g = rng.normal(0, .3, m), rng.normal(0, .3, n)
+        gf, gg = po.dual_gradient(f, g, C, a, b, eta)
+        h = 1e-6
+        for i in range(m):
+            e = np.zeros(m); e[i] = h
+            fd = (po.dual_objective(f + e, g, C, a, b, eta) - po.dual_objective(f - e, g, C, a, b, eta)) / (2 * h)
+            assert abs(fd - gf[i]) <= 1e-6 * (1 + abs(gf).max())
+        for j in range(n):
+            e = np.zeros(n); e[j] = h
+            fd = (po.dual_objective(f, g + e, C, a, b, eta) - po.dual_objective(f, g - e, C, a, b, eta)) / (2 * h)
+            assert abs(fd - gg[j]) <= 1e-6 * (1 + abs(gg).max())
+
+
+@pytest.mark.parametrize("eta", [1.0, 0.1])
+def test_hessian_matches_finite_differences(eta):
+    rng = np.random.default_rng(12)
+    for _ in range(10):
+        m, n = rng.integers(2, 7), rng.integers(2, 6)
+        C = rng.random((m, n)); a = po_norm(rng.random(m) + .1); b = po_norm(rng.random(n) + .1)
+        f, g = rng.normal(0, .3, m), rng.normal(0, .3, n)
+        H = po.hessian_dense(f, g, C, eta)
+        h = 1e-5
+        for k in range(m + n):
+            d = np.zeros(m + n); d[k] = h
+            gp = np.concatenate(po.dual_gradient(f + d[:m], g + d[m:], C, a, b, eta))
+            gm = np.concatenate(po.dual_gradient(f - d[:m], g - d[m:], C, a, b, eta))
+            fd = (gp - gm) / (2 * h)
+            assert np.abs(fd - H[:, k]).max() <= 1e-5 * (1 + np.abs(H).max())
+
+
+def test_hessian_null_vector():
+    # Eq. (9): [[diag(Xe), X],[X^T, diag(X^T e)]] (e_m, -e_n) = 0
+    rng = np.random.default_rng(3)
+    C = rng.random((5, 4)); f, g = rng.normal(size=5), rng.normal(size=4)
+    H = po.hessian_dense(f, g, C, 0.5)
+    z = np.concatenate([np.ones(5), -np.ones(4)])
+    assert np.abs(H @ z).max() <= 1e-12 * np.abs(H).max()
+
+
+def po_norm(v):
+    return v / v.sum()
+
+
+# ------------------------------------------------------------------- Sinkhorn
+def test_sinkhorn_marginals_exact_after_updates():
+    # Alg. 2 line 5: after the f-update the rows of X~(f^{t+1}, g^t) sum to a;
+    # line 6: after the g-update the columns sum to b.
+    rng = np.random.default_rng(8)
+    C = rng.random((10, 10)); a = po_norm(rng.random(10) + .1); b = po_norm(rng.random(10) + .1)
+    f, g = np.zeros(10), np.zeros(10)
+    prev = -np.inf
+    for _ in range(200):
+        f1, g1 = po.sinkhorn_sweep(f, g, C, a, b, 0.05)
+        rows = po.plan(f1, g, C, 0.05).sum(1)
+        assert np.abs(rows - a).sum() <= 1e-12
+        cols = po.plan(f1, g1, C, 0.05).sum(0)
+        assert np.abs(cols - b).sum() <= 1e-12
+        P = po.dual_objective(f1, g1, C, a, b, 0.05)
+        assert P >= prev - 1e-12          # exact alternating maximisation
+        prev, f, g = P, f1, g1
+
+
+def test_sinkhorn_constant_cost_gives_product_plan():
+    # C = c E: one sweep lands on X = a b^T (rank-one scaling stays rank one)
+    rng = np.random.default_rng(1)
+    a = po_norm(rng.random(6) + .1); b = po_norm(rng.random(4) + .1)
+    C = np.full((6, 4), 0.37)
+    f, g = po.sinkhorn_sweep(np.zeros(6), np.zeros(4), C, a, b, 0.1)
+    assert np.allclose(po.plan(f, g, C, 0.1), np.outer(a, b), rtol=1e-13, atol=0)
+
+
+def test_sinkhorn_single_cell():
+    f, g = po.sinkhorn_sweep(np.zeros(1), np.zeros(1), np.array([[0.4]]), np.ones(1), np.ones(1), 0.01)
+    assert abs(po.plan(f, g, np.array([[0.4]]), 0.01)[0, 0] - 1.0) < 1e-14
+
+
+# ------------------------------------------------------------- sparsify / CG
+def test_sparsify_threshold_and_topk():
+    P = np.array([[4.0, 1.0], [3.0, 2.0]])
+    assert (po.sparsify_topk(P, 0.5) == np.array([[True, False], [True, False]])).all()
+    assert po.sparsify_topk(P, 1.0).all()
+    assert (po.sparsify_threshold(P, 2.0) == np.array([[True, False], [True, True]])).all()
+    rp, ci, v = po.csr_from_mask(P, po.sparsify_threshold(P, 2.0))
+    assert list(rp) == [0, 1, 3] and list(ci) == [0, 0, 1] and list(v) == [4.0, 3.0, 2.0]
+
+
+def test_cg_small_spd():
+    A = np.array([[4.0, 1.0], [1.0, 3.0]])
+    x, its, res = po.cg(lambda p: A @ p, np.array([1.0, 2.0]), 1e-14, 10)
+    assert np.allclose(x, [1 / 11, 7 / 11], atol=1e-14)
+    rng = np.random.default_rng(2)
+    B = rng.normal(size=(30, 30)); A = B @ B.T + 30 * np.eye(30); rhs = rng.normal(size=30)
+    x, its, res = po.cg(lambda p: A @ p, rhs, 1e-12, 200, diag=np.diag(A))
+    assert np.allclose(x, np.linalg.solve(A, rhs), rtol=1e-9, atol=1e-12)
+
+
+def test_line_search_quadratic_accepts_unit_step():
+    # P(x) = -(x-1)^2 at x=0, d=1: alpha = 1 is accepted (SPEC example, §3.2)
+    P = lambda x: -(x - 1.0) ** 2
+    x, d, c = 0.0, 1.0, 1e-4
+    assert P(x + d) >= P(x) + c * 1.0 * 2.0 * d
+
+
+def test_newton_direction_is_exact_newton_without_sparsification():
+    # With theta = 0 (keep everything), mu -> 0 and a tight CG, the direction
+    # solves the Newton system of Eq. (9):  hess P d = -grad P  (min-norm sense).
+    rng = np.random.default_rng(4)
+    m, n, eta = 6, 5, 0.2
+    C = rng.random((m, n)); a = po_norm(rng.random(m) + .1); b = po_norm(rng.random(n) + .1)
+    f, g = np.zeros(m), np.zeros(n)
+    for _ in range(5):
+        f, g = po.sinkhorn_sweep(f, g, C, a, b, eta)
+    prm = po.Params(theta=0.0, cg_tol=1e-12, cg_forcing=0.0, cg_maxit=500)
+    df, dg, info = po.newton_direction(f, g, C, a, b, eta, prm)
+    H = po.hessian_dense(f, g, C, eta)
+    grad = np.concatenate(po.dual_gradient(f, g, C, a, b, eta))
+    d = np.concatenate([df, dg])
+    assert np.abs(H @ d + grad).max() <= 1e-10
+    # quadratic convergence: two Newton steps shrink the gradient sharply
+    res0 = np.abs(grad).sum()
+    f1, g1, _ = po.newton_step(f, g, C, a, b, eta, prm)
+    f2, g2, _ = po.newton_step(f1, g1, C, a, b, eta, prm)
+    assert po.residual_l1(f2, g2, C, a, b, eta) < 1e-4 * res0
+
+
+# ------------------------------------------------------------------ PINS (Alg. 2)
+def test_pins_identity_with_annealed_entropic_ot():
+    # Eq. (5)-(7): with X^0 = a b^T and subproblems solved to high accuracy,
+    # X^{k} = argmin <C,X> + (eta/k) sum X log X over the polytope (the shifted
+    # costs C^k are k C up to separable terms).  Independent check: plain
+    # Sinkhorn on C with regularisation eta/k.
+    rng = np.random.default_rng(9)
+    m, n, eta, K = 7, 6, 0.2, 4
+    C = rng.random((m, n)); a = po_norm(rng.random(m) + .1); b = po_norm(rng.random(n) + .1)
+    prm = po.Params(eta=eta, K=K, outer_tol=0.0, sink_tol=1e-13, T1=100000, newton_tol=1e-14)
+    r = po.pins(C, a, b, prm)
+    epsk = eta / K
+    f, g = np.zeros(m), np.zeros(n)
+    for _ in range(20000):
+        f, g = po.sinkhorn_sweep(f, g, C, a, b, epsk)
+    Xent = po.plan(f, g, C, epsk)
+    assert np.abs(np.exp(r.logX) - Xent).max() <= 1e-9
+
+
+def test_pins_uniform_square_matches_brute_force():
+    rng = np.random.default_rng(21)
+    for n in (3, 5, 6):
+        C = rng.random((n, n)); a = np.full(n, 1.0 / n)
+        _, opt = brute_force_assignment(C)
+        prm = po.Params(eta=0.05, K=4000, outer_rule=1, outer_tol=1e-8, newton_tol=1e-12)
+        r = po.pins(C, a, a.copy(), prm, trace=True)
+        assert abs(r.obj - opt) <= 1e-7 * abs(opt)
+        assert r.kkt["primal"] <= 1e-8
+        objs = [t["obj"] for t in r.trace]
+        # Thm 4.1 proof: <C,X^{k+1}> <= <C,X^k>
+        assert all(objs[i + 1] <= objs[i] + 1e-12 for i in range(len(objs) - 1)), max(np.diff(objs))
+
+
+def test_pins_rectangular_matches_network_simplex_and_bregman_monotone():
+    rng = np.random.default_rng(22)
+    m, n = 9, 7
+    C = rng.random((m, n)); a = po_norm(rng.random(m) + .1); b = po_norm(rng.random(n) + .1)
+    ex = solve_exact(C, a, b)
+    prm = po.Params(eta=0.05, K=3000, outer_rule=1, outer_tol=1e-8, newton_tol=1e-12)
+    r = po.pins(C, a, b, prm, trace=True)
+    assert abs(r.obj - ex["obj"]) <= 1e-7 * abs(ex["obj"])
+    # Bregman monotonicity toward X* (Thm 4.1 proof): re-run
+    # the outer loop step by step and track D(X*, X^k)
+    Xs = ex["X"]
+    prm2 = po.Params(eta=0.05, K=1, outer_tol=0.0, newton_tol=1e-13)
+    logX = np.log(a)[:, None] + np.log(b)[None, :]
+    f, g = np.zeros(m), np.zeros(n)
+    prev = po.bregman(Xs, np.exp(logX))
+    for _ in range(30):
+        Ck = po.shifted_cost(C, logX, 0.05)
+        for _ in range(200):
+            f, g = po.sinkhorn_sweep(f, g, Ck, a, b, 0.05)
+        for _ in range(5):
+            f, g, _ = po.newton_step(f, g, Ck, a, b, 0.05, prm2)
+        logX = po.log_plan(f, g, Ck, 0.05)
+        D = po.bregman(Xs, np.exp(logX))
+        assert D <= prev + 1e-9
+        prev = D
+
+
+def test_kkt_of_exact_solution_is_zero():
+    rng = np.random.default_rng(23)
+    C = rng.random((6, 8)); a = po_norm(rng.random(6) + .1); b = po_norm(rng.random(8) + .1)
+    ex = solve_exact(C, a, b)
+    X = ex["X"]
+    assert np.abs(X.sum(1) - a).sum() + np.abs(X.sum(0) - b).sum() <= 1e-14
+    assert (ex["u"][:, None] + ex["v"][None, :] - C).max() <= 1e-12
+    assert abs((C * X).sum() - a @ ex["u"] - b @ ex["v"]) <= 1e-13
+
+
+def test_outer_rules():
+    prm = po.Params(outer_rule=0, outer_tol=1e-4)
+    assert po.outer_converged([1.0, 1.0], prm)
+    assert not po.outer_converged([1.0, 0.99989], prm)   # SPEC example: change 1.1e-4
+    prm1 = po.Params(outer_rule=1, outer_tol=1e-3)
+    seq = [1 + 1.0 / (k + 1) for k in range(4000)]
+    k_stop = next(k for k in range(2, 4000) if po.outer_converged(seq[:k], prm1))
+    # error 1/k halves when k doubles: the halving estimate is exact for 1/k
+    assert abs(1.0 / k_stop - 1e-3) < 2e-4
