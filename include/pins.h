@@ -1,0 +1,194 @@
+/*
+ * pins.h -- C ABI of libpins_b200.so: the PINS hot path (arXiv 2502.03749,
+ * "PINS: Proximal Iterations with Sparse Newton and Sinkhorn for Optimal
+ * Transport") on one B200 (sm_100a).
+ *
+ * Conventions (all entry points):
+ *  - Every array argument is a DEVICE pointer to fp64 (or int32 / int64 where
+ *    stated) memory owned by the caller, unless the name ends in _host.  The
+ *    library never frees caller memory.  Scratch memory is owned by a
+ *    pins_workspace (stream-ordered allocations on the stream passed in).
+ *  - `stream` is a cudaStream_t passed as void*; NULL means the legacy default
+ *    stream.  Calls are asynchronous w.r.t. the host unless they return host
+ *    scalars (documented per call), which synchronise `stream`.
+ *  - Return value: PINS_OK (0) or a PINS_ERR_* code; nothing is thrown.  On a
+ *    CUDA error the sticky error text is available from pins_last_error().
+ *
+ * Problem (Eq. (1), lines 41-46):  min <C,X>  s.t.  X e_n = a,
+ * X^T e_m = b, X >= 0, with C given either densely or by point coordinates:
+ *    C_ij = cost_scale * D_ij,
+ *    D_ij = C[i*ldc + j]                       (PINS_COST_DENSE)
+ *         = sum_k (x[i*d+k] - y[j*d+k])^2     (PINS_COST_SQEUCLID)
+ *         = sum_k |x[i*d+k] - y[j*d+k]|       (PINS_COST_L1)
+ * Point kinds recompute D on the fly inside every dense pass (no m x n array).
+ *
+ * Proximal centre (Eq. (5)-(7), Alg. 2 lines 3 and 16) in factored
+ * log form:  C^k = s C - phi (+) psi, i.e.
+ *    log X^k_ij = (phi_i + psi_j - s C_ij)/eta        (X^0 = a b^T: s=1,
+ *    phi = eta log a, psi = eta log b).
+ * Subproblem potentials (f, g) are the paper's; the plan of Eq. (7) is
+ *    X~_ij = exp((f_i + phi_i + g_j + psi_j - s C_ij)/eta - 1).
+ */
+#ifndef PINS_B200_H
+#define PINS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PINS_OK 0
+#define PINS_ERR_ARG 1        /* invalid argument (sizes, NULL pointers, kinds) */
+#define PINS_ERR_CUDA 2       /* CUDA runtime error (see pins_last_error)        */
+#define PINS_ERR_NOMEM 3      /* device allocation failed                        */
+#define PINS_ERR_NUMERIC 4    /* non-finite value where a finite one is required */
+
+#define PINS_COST_DENSE 0
+#define PINS_COST_SQEUCLID 1
+#define PINS_COST_L1 2
+
+typedef struct pins_problem {
+    int64_t m, n;            /* sizes, m >= 1, n >= 1                              */
+    int32_t cost_kind;       /* PINS_COST_*                                        */
+    int32_t d;               /* point dimension (1..16) for point kinds            */
+    const double *C;         /* DENSE: device m x n, row-major, leading dim ldc    */
+    int64_t ldc;             /* >= n                                               */
+    const double *x;         /* points: device m x d row-major (integer-valued for */
+    const double *y;         /*   exact costs; any finite values are accepted)     */
+    double cost_scale;       /* C_ij = cost_scale * D_ij  (> 0)                    */
+    const double *a;         /* device m, > 0, sum 1                               */
+    const double *b;         /* device n, > 0, sum 1                               */
+    double eta;              /* entropic / proximal parameter, > 0                 */
+} pins_problem;
+
+/* Solver parameters; semantics identical to oracle/pins_oracle.py Params.
+ * Defaults (pins_default_params) follow PAPER.md Appendix A.2 (lines 477-485). */
+typedef struct pins_params {
+    int32_t K;               /* max EPPA (outer) iterations               (500)   */
+    int32_t outer_rule;      /* 0 rel. change, 1 halving, 2 geometric tail (0)   */
+    double outer_tol;        /* outer tolerance                           (1e-4)  */
+    int32_t T1;              /* max Sinkhorn sweeps per subproblem        (50000) */
+    double sink_tol;         /* Sinkhorn phase: ||grad P||_1 threshold    (6.3e-4)*/
+    int32_t T2;              /* max Newton iterations per subproblem      (20)    */
+    double newton_tol;       /* Newton phase: ||grad P||_1 threshold      (1e-8)  */
+    double theta;            /* sparsify: keep X~_ij >= theta/(m n)       (1e-4)  */
+    double cg_tol;           /* CG relative-residual floor                (1e-6)  */
+    double cg_forcing;       /* rtol = clamp(cg_forcing*newton_tol/||g||_1, cg_tol, 0.5) (0.1) */
+    int32_t cg_maxit;        /* (1000) */
+    double mu_rel;           /* damping mu = mu_rel * max diagonal        (1e-10) */
+    double armijo_c;         /* (1e-4) */
+    double beta;             /* backtracking factor (0.5) */
+    int32_t max_backtracks;  /* (30) */
+    int32_t warm_start;      /* 1 carry (f,g) across outer iterations      (1)    */
+} pins_params;
+
+void pins_default_params(pins_params *p);
+
+/* Opaque scratch owner (row buffers, CSR/CSC, column partials, CG vectors). */
+typedef struct pins_workspace pins_workspace;
+int pins_workspace_create(pins_workspace **ws);
+void pins_workspace_destroy(pins_workspace *ws);
+
+/* Last error message for this thread (static storage, never NULL). */
+const char *pins_last_error(void);
+
+/* Initialise the proximal centre to X^0 = a b^T: s=1, phi = eta log a,
+ * psi = eta log b.  phi (m), psi (n) device, caller-owned.                   */
+int pins_center_init(const pins_problem *pb, double *phi, double *psi, double *s_host,
+                     void *stream);
+
+/* Proximal-centre update, Alg. 2 line 16 then line 3:
+ * X^{k+1} = X~(f, g) in log form:  phi += f,  psi += g - eta,  s += 1.       */
+int pins_center_update(const pins_problem *pb, double *phi, double *psi, double *s_host,
+                       const double *f, const double *g, void *stream);
+
+/* One log-domain Sinkhorn sweep in place, Alg. 2 lines 5-6:
+ *   f <- eta(log a + 1) - eta LSE_j((g_j - C^k_ij)/eta)
+ *   g <- eta(log b + 1) - eta LSE_i((f_i - C^k_ij)/eta)   (with the new f).
+ * Fused row-then-column kernel + column finalize.  Asynchronous.             */
+int pins_sinkhorn_sweep(pins_workspace *ws, const pins_problem *pb, const double *phi,
+                        const double *psi, double s, double *f, double *g, void *stream);
+
+/* Evaluation pass at (f, g): plan X~ of Eq. (7), its row sums r (m) and column
+ * sums c (n) (either may be NULL), the gradient norm and objectives.  Host
+ * scalars (synchronises):  out_host[0] = ||a - r||_1 + ||b - c||_1 (= ||grad
+ * P^k||_1, Eq. (9)),  [1] = sum X~,  [2] = <C, X~>,  [3] = P^k(f,g) (Eq. (8)).
+ * If tau > 0 the plan block is also sparsified (X~_ij >= tau) into the
+ * workspace CSR, and out_host[4] = nnz.                                       */
+int pins_evaluate(pins_workspace *ws, const pins_problem *pb, const double *phi,
+                  const double *psi, double s, const double *f, const double *g,
+                  double tau, double *r, double *c, double *out_host, void *stream);
+
+/* The CSR produced by the last pins_evaluate(tau > 0) / pins_newton_step
+ * (Alg. 2 line 11, reading R3): row-major, columns
+ * ascending, entries X~_ij >= tau.  *nnz_host, *m_host receive the sizes;
+ * if rowptr (m+1, int64), colidx (int32) and val (fp64) are non-NULL the CSR
+ * is copied into them (cap >= nnz required, else PINS_ERR_ARG).  Synchronises. */
+int pins_get_csr(pins_workspace *ws, int64_t *rowptr, int32_t *colidx, double *val, int64_t cap,
+                 int64_t *nnz_host, int64_t *m_host);
+
+/* Sparsify a caller-given dense plan block P (device m x n, leading dim ldp)
+ * with the same compaction kernel: CSR of P_ij >= tau (PAPER.md:255-256,
+ * reading R3).  Output as pins_get_csr.  Synchronises.                       */
+int pins_sparsify_dense(pins_workspace *ws, int64_t m, int64_t n, const double *P, int64_t ldp,
+                        double tau, int64_t *rowptr, int32_t *colidx, double *val, int64_t cap,
+                        int64_t *nnz_host, void *stream);
+
+/* Jacobi-preconditioned CG (reading R5) on
+ *   M = [[diag(dr) , Xs ], [Xs^T, diag(dc)]] + mu I,   M x = rhs
+ * with Xs given as CSR (rowptr int64 m+1, colidx int32, val fp64, nnz).
+ * rhs, x: device (m+n); x is overwritten (start 0).  One cooperative
+ * persistent launch; iterations and final relative residual returned on the
+ * host (synchronises).                                                        */
+int pins_cg(pins_workspace *ws, int64_t m, int64_t n, const int64_t *rowptr,
+            const int32_t *colidx, const double *val, int64_t nnz, const double *dr,
+            const double *dc, double mu, const double *rhs, double *x, double rtol,
+            int32_t maxit, int32_t *iters_host, double *relres_host, void *stream);
+
+/* One sparse Newton iteration on subproblem k, Alg. 2 lines 10-14
+ * (PAPER.md:173-180): evaluate + sparsify (tau = theta/(mn)), CG on the
+ * sparsified Hessian, backtracking line search, update (f, g) in place.
+ * info_host: [0] grad l1 before, [1] grad l1 after, [2] alpha, [3] CG iters,
+ * [4] CG rel. residual, [5] nnz, [6] line-search trials.  Synchronises.       */
+int pins_newton_step(pins_workspace *ws, const pins_problem *pb, const pins_params *prm,
+                     const double *phi, const double *psi, double s, double *f, double *g,
+                     double *info_host, void *stream);
+
+/* LP residuals of the plan X~(f,g) at centre (phi,psi,s) (reading R8):
+ * res_host[0] = ||Xe-a||_1 + ||X^Te-b||_1, [1] = max(0, max_ij u_i+v_j-C_ij)
+ * with u = (f+phi)/s, v = (g+psi-eta)/s, [2] = <C,X>, [3] = <a,u>+<b,v>,
+ * [4] = [2]-[3].  u, v (device m, n) written if non-NULL.  Synchronises.     */
+int pins_residuals(pins_workspace *ws, const pins_problem *pb, const double *phi,
+                   const double *psi, double s, const double *f, const double *g,
+                   double *u, double *v, double *res_host, void *stream);
+
+/* Materialise X~(f,g) densely (device m x n, leading dim ldx).  Asynchronous. */
+int pins_plan(const pins_problem *pb, const double *phi, const double *psi, double s,
+              const double *f, const double *g, double *X, int64_t ldx, void *stream);
+
+/* Output of pins_solve.  Device arrays are caller-owned (f, g, phi, psi: sizes
+ * m, n, m, n; u, v optional).  Scalars are written on the host.              */
+typedef struct pins_result {
+    double *f, *g;           /* last subproblem potentials (device)              */
+    double *phi, *psi;       /* proximal centre log form (device)                */
+    double *u, *v;           /* LP dual estimates (device, may be NULL)          */
+    double s;                /* centre scale s_K                                 */
+    double obj;              /* <C, X>  (primal objective of the returned plan)  */
+    double dual_obj;         /* P^k(f,g) of the last subproblem (Eq. (8))        */
+    double lp_dual_obj;      /* <a,u> + <b,v>                                    */
+    double kkt;              /* ||Xe-a||_1 + ||X^Te-b||_1  (reading R8)          */
+    double dual_inf;         /* max(0, max_ij u_i + v_j - C_ij)                  */
+    double gap;              /* obj - lp_dual_obj                                */
+    int32_t outer_iters, sweeps, newton_iters, cg_iters, status; /* status 0 = converged, 1 = budget */
+    double *obj_trace_host;  /* optional host array of length >= K (may be NULL) */
+    double seconds;          /* host wall time of the solve                      */
+} pins_result;
+
+/* Full PINS solve, Algorithm 2.  Synchronises.            */
+int pins_solve(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PINS_B200_H */

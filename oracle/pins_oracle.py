@@ -304,6 +304,9 @@ class Result:
     dual_obj: float
     kkt: Dict[str, float]
     outer_iters: int
+    phi: np.ndarray          # eta log a + sum_t f^t      (centre of the next subproblem:
+    psi: np.ndarray          # eta log b + sum_t (g^t-eta)  C^K = s_next C - phi (+) psi)
+    s_next: float
     sweeps: int
     newton_iters: int
     cg_iters: int
@@ -370,7 +373,8 @@ def pins(C: np.ndarray, a: np.ndarray, b: np.ndarray, prm: Params, trace: bool =
     v = gsum / s
     dual = dual_objective(f, g, Ck, a, b, eta)
     return Result(logX=logX, f=f, g=g, u=u, v=v, obj=objs[-1], dual_obj=dual,
-                  kkt=kkt(C, logX, a, b, u, v), outer_iters=k + 1, sweeps=sweeps,
+                  kkt=kkt(C, logX, a, b, u, v), outer_iters=k + 1, phi=fsum, psi=gsum,
+                  s_next=float(k + 2), sweeps=sweeps,
                   newton_iters=newton_its, cg_iters=cg_its, trace=tr)
 
 

@@ -1,0 +1,854 @@
+// pins_api.cu -- C ABI of libpins_b200.so (include/pins.h): workspace, kernel
+// launchers, the Newton step and the host-driven PINS loop (Algorithm 2).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "pins.h"
+#include "pins_kernels.cuh"
+
+using namespace pins;
+
+static thread_local char g_err[512] = "ok";
+extern "C" const char *pins_last_error(void) { return g_err; }
+
+#define PINS_CUDA(x)                                                                        \
+    do {                                                                                    \
+        cudaError_t e_ = (x);                                                               \
+        if (e_ != cudaSuccess) {                                                            \
+            snprintf(g_err, sizeof g_err, "%s:%d %s -> %s", __FILE__, __LINE__, #x,        \
+                     cudaGetErrorString(e_));                                               \
+            return PINS_ERR_CUDA;                                                           \
+        }                                                                                   \
+    } while (0)
+#define PINS_TRY(x)                    \
+    do {                               \
+        int rc_ = (x);                 \
+        if (rc_ != PINS_OK) return rc_; \
+    } while (0)
+#define PINS_ARG(cond, msg)                                              \
+    do {                                                                 \
+        if (!(cond)) {                                                   \
+            snprintf(g_err, sizeof g_err, "invalid argument: %s", msg); \
+            return PINS_ERR_ARG;                                         \
+        }                                                                \
+    } while (0)
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+int ensure(DevBuf &b, size_t bytes) {
+    if (bytes == 0) bytes = 8;
+    if (b.bytes >= bytes) return PINS_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e != cudaSuccess) {
+        snprintf(g_err, sizeof g_err, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+        return PINS_ERR_NOMEM;
+    }
+    b.bytes = bytes;
+    return PINS_OK;
+}
+
+template <class T>
+T *ptr(DevBuf &b) { return reinterpret_cast<T *>(b.p); }
+
+}  // namespace
+
+struct pins_workspace {
+    DevBuf colpart, blk, rowsum, gradf, colsum, gradg, rowcnt, rb_col, rb_val;
+    DevBuf rowptr, colidx, val, colcnt, colptr, cursor, rowidx, valT;
+    DevBuf cgvec, cgpart, cgst, st, ft, gt, eu, ev, dir, rhs, tab, fsave, gsave, uv;
+    long long m = 0, n = 0, cap = 64, nnz = 0;
+    int G = 0, nsm = 0, dev = -1;
+    bool csr_ready = false, csc_ready = false;
+    double *h = nullptr;   // pinned host scalars (64)
+};
+
+extern "C" void pins_default_params(pins_params *p) {
+    p->K = 500;
+    p->outer_rule = 0;
+    p->outer_tol = 1e-4;
+    p->T1 = 50000;
+    p->sink_tol = 6.3e-4;
+    p->T2 = 20;
+    p->newton_tol = 1e-8;
+    p->theta = 1e-4;
+    p->cg_tol = 1e-6;
+    p->cg_forcing = 0.1;
+    p->cg_maxit = 1000;
+    p->mu_rel = 1e-10;
+    p->armijo_c = 1e-4;
+    p->beta = 0.5;
+    p->max_backtracks = 30;
+    p->warm_start = 1;
+}
+
+extern "C" int pins_workspace_create(pins_workspace **out) {
+    PINS_ARG(out != nullptr, "ws");
+    pins_workspace *ws = new pins_workspace();
+    PINS_CUDA(cudaGetDevice(&ws->dev));
+    PINS_CUDA(cudaDeviceGetAttribute(&ws->nsm, cudaDevAttrMultiProcessorCount, ws->dev));
+    PINS_CUDA(cudaMallocHost(&ws->h, 64 * sizeof(double)));
+    // exp table 2^(j/64), hi + lo, from 80-bit long double
+    ExpTable t;
+    for (int j = 0; j < 64; ++j) {
+        long double v = exp2l((long double)j / 64.0L);
+        t.hi[j] = (double)v;
+        t.lo[j] = (double)(v - (long double)t.hi[j]);
+    }
+    PINS_TRY(ensure(ws->tab, sizeof(ExpTable)));
+    PINS_CUDA(cudaMemcpy(ws->tab.p, &t, sizeof t, cudaMemcpyHostToDevice));
+    *out = ws;
+    return PINS_OK;
+}
+
+extern "C" void pins_workspace_destroy(pins_workspace *ws) {
+    if (!ws) return;
+    DevBuf *bufs[] = {&ws->colpart, &ws->blk, &ws->rowsum, &ws->gradf, &ws->colsum, &ws->gradg,
+                      &ws->rowcnt, &ws->rb_col, &ws->rb_val, &ws->rowptr, &ws->colidx, &ws->val,
+                      &ws->colcnt, &ws->colptr, &ws->cursor, &ws->rowidx, &ws->valT, &ws->cgvec,
+                      &ws->cgpart, &ws->cgst, &ws->st, &ws->ft, &ws->gt, &ws->eu, &ws->ev,
+                      &ws->dir, &ws->rhs, &ws->tab, &ws->fsave, &ws->gsave, &ws->uv};
+    for (DevBuf *b : bufs)
+        if (b->p) cudaFree(b->p);
+    if (ws->h) cudaFreeHost(ws->h);
+    delete ws;
+}
+
+namespace {
+
+int check_problem(const pins_problem *pb) {
+    PINS_ARG(pb != nullptr, "problem");
+    PINS_ARG(pb->m >= 1 && pb->n >= 1, "m, n >= 1");
+    PINS_ARG(pb->n < (1LL << 31) && pb->m < (1LL << 31), "m, n < 2^31");
+    PINS_ARG(pb->a && pb->b, "a, b");
+    PINS_ARG(pb->eta > 0.0 && std::isfinite(pb->eta), "eta > 0");
+    PINS_ARG(pb->cost_scale > 0.0 && std::isfinite(pb->cost_scale), "cost_scale > 0");
+    if (pb->cost_kind == PINS_COST_DENSE) {
+        PINS_ARG(pb->C != nullptr && pb->ldc >= pb->n, "dense C / ldc");
+    } else {
+        PINS_ARG(pb->cost_kind == PINS_COST_SQEUCLID || pb->cost_kind == PINS_COST_L1, "cost_kind");
+        PINS_ARG(pb->x && pb->y && pb->d >= 1 && pb->d <= 16, "points x, y, 1 <= d <= 16");
+    }
+    return PINS_OK;
+}
+
+CostDesc make_cd(const pins_problem *pb) {
+    CostDesc cd;
+    cd.kind = pb->cost_kind;
+    cd.d = pb->d;
+    cd.C = pb->C;
+    cd.ldc = pb->ldc;
+    cd.x = pb->x;
+    cd.y = pb->y;
+    cd.vec2 = (pb->cost_kind == PINS_COST_DENSE || pb->cost_kind == 3) &&
+              ((reinterpret_cast<uintptr_t>(pb->C) & 15) == 0) && (pb->ldc % 2 == 0);
+    return cd;
+}
+
+int dmax_for(int d) { return d <= 2 ? 2 : d <= 3 ? 3 : d <= 10 ? 10 : 16; }
+
+template <bool SP, bool TR>
+cudaError_t launch_eval_t(int kind, int d, int G, cudaStream_t st, const EvalArgs &A) {
+    dim3 grid(G), block(kThreads);
+    const int dm = dmax_for(d);
+    if (kind == 0) eval_kernel<0, 0, SP, TR><<<grid, block, 0, st>>>(A);
+    else if (kind == 3) {
+        if constexpr (SP && !TR) eval_kernel<3, 0, true, false><<<grid, block, 0, st>>>(A);
+    } else if (kind == 1) {
+        if (dm == 2) eval_kernel<1, 2, SP, TR><<<grid, block, 0, st>>>(A);
+        else if (dm == 3) eval_kernel<1, 3, SP, TR><<<grid, block, 0, st>>>(A);
+        else if (dm == 10) eval_kernel<1, 10, SP, TR><<<grid, block, 0, st>>>(A);
+        else eval_kernel<1, 16, SP, TR><<<grid, block, 0, st>>>(A);
+    } else {
+        if (dm == 2) eval_kernel<2, 2, SP, TR><<<grid, block, 0, st>>>(A);
+        else if (dm == 3) eval_kernel<2, 3, SP, TR><<<grid, block, 0, st>>>(A);
+        else if (dm == 10) eval_kernel<2, 10, SP, TR><<<grid, block, 0, st>>>(A);
+        else eval_kernel<2, 16, SP, TR><<<grid, block, 0, st>>>(A);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval(bool sp, bool tr, int kind, int d, int G, cudaStream_t st, const EvalArgs &A) {
+    if (sp && tr) return launch_eval_t<true, true>(kind, d, G, st, A);
+    if (sp) return launch_eval_t<true, false>(kind, d, G, st, A);
+    if (tr) return launch_eval_t<false, true>(kind, d, G, st, A);
+    return launch_eval_t<false, false>(kind, d, G, st, A);
+}
+
+template <template <int, int> class K>
+struct Dummy {};
+
+cudaError_t launch_sweep(int kind, int d, long long m, long long n, cudaStream_t st, int nsm,
+                         const SweepArgs &A) {
+    const int dm = dmax_for(d);
+    const int rows_blocks = (int)std::min<long long>((m + kWarps - 1) / kWarps, (long long)nsm * 16);
+    const int col_blocks = (int)std::min<long long>((n + 31) / 32, (long long)nsm * 8);
+#define SWEEP_PAIR(KD, DM)                                                  \
+    do {                                                                    \
+        sweep_row_kernel<KD, DM><<<rows_blocks, kThreads, 0, st>>>(A);     \
+        sweep_col_kernel<KD, DM><<<col_blocks, kThreads, 0, st>>>(A);      \
+    } while (0)
+    if (kind == 0) SWEEP_PAIR(0, 0);
+    else if (kind == 1) {
+        if (dm == 2) SWEEP_PAIR(1, 2);
+        else if (dm == 3) SWEEP_PAIR(1, 3);
+        else if (dm == 10) SWEEP_PAIR(1, 10);
+        else SWEEP_PAIR(1, 16);
+    } else {
+        if (dm == 2) SWEEP_PAIR(2, 2);
+        else if (dm == 3) SWEEP_PAIR(2, 3);
+        else if (dm == 10) SWEEP_PAIR(2, 10);
+        else SWEEP_PAIR(2, 16);
+    }
+#undef SWEEP_PAIR
+    return cudaGetLastError();
+}
+
+int grid_1d(long long work, int nsm, int per_sm = 8) {
+    long long g = (work + 255) / 256;
+    if (g < 1) g = 1;
+    return (int)std::min<long long>(g, (long long)nsm * per_sm);
+}
+
+// choose the eval grid: balanced row ranges, <= kRMax rows per CTA
+int eval_grid(long long m, int nsm) {
+    const long long slots = (long long)nsm * 2;
+    long long waves = (m + kRMax * slots - 1) / (kRMax * slots);
+    long long G = slots * std::max<long long>(waves, 1);
+    G = std::min(G, m);
+    G = std::max(G, (m + kRMax - 1) / kRMax);
+    return (int)G;
+}
+
+int prepare(pins_workspace *ws, const pins_problem *pb) {
+    const long long m = pb->m, n = pb->n;
+    if (ws->m != m || ws->n != n) {
+        ws->m = m;
+        ws->n = n;
+        ws->csr_ready = ws->csc_ready = false;
+    }
+    ws->G = eval_grid(m, ws->nsm);
+    const long long N = m + n;
+    PINS_TRY(ensure(ws->colpart, sizeof(double) * ws->G * n));
+    PINS_TRY(ensure(ws->blk, sizeof(double) * ws->G * 4));
+    PINS_TRY(ensure(ws->rowsum, sizeof(double) * m));
+    PINS_TRY(ensure(ws->gradf, sizeof(double) * m));
+    PINS_TRY(ensure(ws->colsum, sizeof(double) * n));
+    PINS_TRY(ensure(ws->gradg, sizeof(double) * n));
+    PINS_TRY(ensure(ws->rowcnt, sizeof(int) * m));
+    PINS_TRY(ensure(ws->st, sizeof(double) * 32));
+    PINS_TRY(ensure(ws->ft, sizeof(double) * m));
+    PINS_TRY(ensure(ws->gt, sizeof(double) * n));
+    PINS_TRY(ensure(ws->eu, sizeof(double) * m));
+    PINS_TRY(ensure(ws->ev, sizeof(double) * n));
+    PINS_TRY(ensure(ws->dir, sizeof(double) * N));
+    PINS_TRY(ensure(ws->rhs, sizeof(double) * N));
+    PINS_TRY(ensure(ws->fsave, sizeof(double) * m));
+    PINS_TRY(ensure(ws->gsave, sizeof(double) * n));
+    PINS_TRY(ensure(ws->uv, sizeof(double) * N));
+    PINS_TRY(ensure(ws->rb_col, sizeof(int) * m * ws->cap));
+    PINS_TRY(ensure(ws->rb_val, sizeof(double) * m * ws->cap));
+    return PINS_OK;
+}
+
+// extra reductions: st[8] = <a,f> + <b,g>, st[9] = max rowsum, st[10] = max colsum
+__global__ void __launch_bounds__(1024) dots_kernel(long long m, long long n, const double *a,
+                                                    const double *f, const double *b,
+                                                    const double *g, const double *rowsum,
+                                                    const double *colsum, double *st) {
+    __shared__ double sh[32][3];
+    double s = 0.0, mr = 0.0, mc = 0.0;
+    for (long long i = threadIdx.x; i < m; i += 1024) {
+        s = fma(a[i], f[i], s);
+        mr = fmax(mr, rowsum[i]);
+    }
+    for (long long j = threadIdx.x; j < n; j += 1024) {
+        s = fma(b[j], g[j], s);
+        mc = fmax(mc, colsum[j]);
+    }
+    s = warp_sum(s);
+    mr = warp_max(mr);
+    mc = warp_max(mc);
+    if ((threadIdx.x & 31) == 0) {
+        sh[threadIdx.x >> 5][0] = s;
+        sh[threadIdx.x >> 5][1] = mr;
+        sh[threadIdx.x >> 5][2] = mc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int w = 0; w < 32; ++w) {
+            t += sh[w][0];
+            a1 = fmax(a1, sh[w][1]);
+            a2 = fmax(a2, sh[w][2]);
+        }
+        st[8] = t;
+        st[9] = a1;
+        st[10] = a2;
+    }
+}
+
+struct EvalOut {
+    double gnorm, sumX, cost, dualP, nnz, maxz, maxcnt, em1, maxr, maxc, af;
+};
+
+// One evaluation pass (+ optional sparsify, + optional trial term).  Grows the
+// row-buffer capacity and re-runs on overflow.  Synchronises the stream.
+int run_eval(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi,
+             double s, const double *f, const double *g, double tau, bool trial,
+             cudaStream_t st, EvalOut *out) {
+    PINS_TRY(prepare(ws, pb));
+    const bool sparse = tau > 0.0;
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        EvalArgs A;
+        A.m = pb->m;
+        A.n = pb->n;
+        A.cd = make_cd(pb);
+        A.f = f;
+        A.phi = phi;
+        A.g = g;
+        A.psi = psi;
+        A.a = pb->a;
+        A.inv_eta = 1.0 / pb->eta;
+        A.w = s * pb->cost_scale / pb->eta;
+        A.tau = tau;
+        A.cap = ws->cap;
+        A.eu = ptr<double>(ws->eu);
+        A.ev = ptr<double>(ws->ev);
+        A.tab = ptr<ExpTable>(ws->tab);
+        A.rowsum = ptr<double>(ws->rowsum);
+        A.gradf = ptr<double>(ws->gradf);
+        A.colpart = ptr<double>(ws->colpart);
+        A.blk = ptr<double>(ws->blk);
+        A.rowcnt = ptr<int>(ws->rowcnt);
+        A.rb_col = ptr<int>(ws->rb_col);
+        A.rb_val = ptr<double>(ws->rb_val);
+        PINS_CUDA(launch_eval(sparse, trial, pb->cost_kind, pb->d, ws->G, st, A));
+        colsum_kernel<<<grid_1d(pb->n, ws->nsm), 256, 0, st>>>(
+            pb->n, ws->G, ptr<double>(ws->colpart), pb->b, ptr<double>(ws->colsum), ptr<double>(ws->gradg));
+        PINS_CUDA(cudaGetLastError());
+        stats_kernel<<<1, 1024, 0, st>>>(pb->m, pb->n, ws->G, ptr<double>(ws->gradf),
+                                         ptr<double>(ws->gradg), ptr<double>(ws->rowsum),
+                                         ptr<double>(ws->blk), sparse ? ptr<int>(ws->rowcnt) : nullptr,
+                                         ws->cap, ptr<double>(ws->st));
+        PINS_CUDA(cudaGetLastError());
+        dots_kernel<<<1, 1024, 0, st>>>(pb->m, pb->n, pb->a, f, pb->b, g, ptr<double>(ws->rowsum),
+                                        ptr<double>(ws->colsum), ptr<double>(ws->st));
+        PINS_CUDA(cudaGetLastError());
+        PINS_CUDA(cudaMemcpyAsync(ws->h, ws->st.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        PINS_CUDA(cudaStreamSynchronize(st));
+        const double *h = ws->h;
+        out->gnorm = h[0] + h[1];
+        out->sumX = h[2];
+        out->cost = h[3] * pb->cost_scale;
+        out->em1 = h[4];
+        out->maxz = h[5];
+        out->maxcnt = h[6];
+        out->nnz = h[7];
+        out->af = h[8];
+        out->maxr = h[9];
+        out->maxc = h[10];
+        out->dualP = h[8] - pb->eta * h[2];
+        ws->csr_ready = ws->csc_ready = false;
+        if (!sparse) return PINS_OK;
+        if (out->maxcnt <= (double)ws->cap) {
+            // CSR from the row buffers
+            PINS_TRY(ensure(ws->rowptr, sizeof(long long) * (pb->m + 1)));
+            const long long nnz = (long long)out->nnz;
+            PINS_TRY(ensure(ws->colidx, sizeof(int) * std::max<long long>(nnz, 1)));
+            PINS_TRY(ensure(ws->val, sizeof(double) * std::max<long long>(nnz, 1)));
+            scan_counts_kernel<<<1, 1024, 0, st>>>(pb->m, ptr<int>(ws->rowcnt), ws->cap,
+                                                   ptr<long long>(ws->rowptr));
+            csr_copy_kernel<<<grid_1d(pb->m * 32, ws->nsm), 256, 0, st>>>(
+                pb->m, ws->cap, ptr<long long>(ws->rowptr), ptr<int>(ws->rb_col),
+                ptr<double>(ws->rb_val), ptr<int>(ws->colidx), ptr<double>(ws->val));
+            PINS_CUDA(cudaGetLastError());
+            ws->nnz = nnz;
+            ws->csr_ready = true;
+            return PINS_OK;
+        }
+        // overflow: grow the per-row capacity and redo the pass
+        long long c = ws->cap;
+        while ((double)c < out->maxcnt) c *= 2;
+        ws->cap = c;
+        PINS_TRY(ensure(ws->rb_col, sizeof(int) * pb->m * ws->cap));
+        PINS_TRY(ensure(ws->rb_val, sizeof(double) * pb->m * ws->cap));
+    }
+    snprintf(g_err, sizeof g_err, "row buffer capacity did not converge");
+    return PINS_ERR_NUMERIC;
+}
+
+int build_csc(pins_workspace *ws, long long m, long long n, const long long *rowptr,
+              const int *colidx, const double *val, long long nnz, cudaStream_t st) {
+    PINS_TRY(ensure(ws->colcnt, sizeof(int) * n));
+    PINS_TRY(ensure(ws->cursor, sizeof(int) * n));
+    PINS_TRY(ensure(ws->colptr, sizeof(long long) * (n + 1)));
+    PINS_TRY(ensure(ws->rowidx, sizeof(int) * std::max<long long>(nnz, 1)));
+    PINS_TRY(ensure(ws->valT, sizeof(double) * std::max<long long>(nnz, 1)));
+    PINS_CUDA(cudaMemsetAsync(ws->colcnt.p, 0, sizeof(int) * n, st));
+    PINS_CUDA(cudaMemsetAsync(ws->cursor.p, 0, sizeof(int) * n, st));
+    const int gw = grid_1d(m * 32, ws->nsm);
+    csc_count_kernel<<<gw, 256, 0, st>>>(m, rowptr, colidx, ptr<int>(ws->colcnt));
+    scan_counts_kernel<<<1, 1024, 0, st>>>(n, ptr<int>(ws->colcnt), 1LL << 40,
+                                           ptr<long long>(ws->colptr));
+    csc_fill_kernel<<<gw, 256, 0, st>>>(m, rowptr, colidx, val, ptr<long long>(ws->colptr),
+                                        ptr<int>(ws->cursor), ptr<int>(ws->rowidx), ptr<double>(ws->valT));
+    csc_sort_kernel<<<grid_1d(n, ws->nsm), 256, 0, st>>>(n, ptr<long long>(ws->colptr),
+                                                         ptr<int>(ws->rowidx), ptr<double>(ws->valT));
+    PINS_CUDA(cudaGetLastError());
+    return PINS_OK;
+}
+
+int cg_blocks(pins_workspace *ws, long long N) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_kernel, kThreads, 0);
+    per_sm = std::max(1, std::min(per_sm, 2));
+    long long want = (N + kThreads - 1) / kThreads;
+    return (int)std::max<long long>(1, std::min<long long>(want, (long long)ws->nsm * per_sm));
+}
+
+// CG launch on the CSR (rowptr/colidx/val) + workspace CSC.  Results in ws->cgst (device).
+int run_cg(pins_workspace *ws, long long m, long long n, const long long *rowptr,
+           const int *colidx, const double *val, const double *dr, const double *dc, double mu,
+           const double *rhs, double *x, double rtol, int maxit, const double *gradf,
+           const double *gradg, const double *a, const double *b, cudaStream_t st) {
+    const long long N = m + n;
+    PINS_TRY(ensure(ws->cgvec, sizeof(double) * 4 * N));
+    const int G = cg_blocks(ws, N);
+    PINS_TRY(ensure(ws->cgpart, sizeof(double) * 4 * G));
+    PINS_TRY(ensure(ws->cgst, sizeof(double) * 8));
+    CGArgs A;
+    A.m = m;
+    A.n = n;
+    A.rowptr = rowptr;
+    A.colidx = colidx;
+    A.val = val;
+    A.colptr = ptr<long long>(ws->colptr);
+    A.rowidx = ptr<int>(ws->rowidx);
+    A.valT = ptr<double>(ws->valT);
+    A.dr = dr;
+    A.dc = dc;
+    A.mu = mu;
+    A.rhs = rhs;
+    A.x = x;
+    double *v = ptr<double>(ws->cgvec);
+    A.r = v;
+    A.z = v + N;
+    A.p = v + 2 * N;
+    A.q = v + 3 * N;
+    A.part = ptr<double>(ws->cgpart);
+    A.rtol = rtol;
+    A.maxit = maxit;
+    A.gradf = gradf;
+    A.gradg = gradg;
+    A.a = a;
+    A.b = b;
+    A.st = ptr<double>(ws->cgst);
+    void *args[] = {&A};
+    PINS_CUDA(cudaLaunchCooperativeKernel((void *)cg_kernel, dim3(G), dim3(kThreads), args, 0, st));
+    return PINS_OK;
+}
+
+double cg_rtol(const pins_params *p, double gnorm) {
+    if (p->cg_forcing <= 0.0 || gnorm <= 0.0) return p->cg_tol;
+    return std::min(0.5, std::max(p->cg_tol, p->cg_forcing * p->newton_tol / gnorm));
+}
+
+// One Newton iteration from the current sparse evaluation state (ws buffers
+// hold X~(f,g) sums, gradient and CSR).  On return the state is that of the
+// new point.  info: [0] gnorm before [1] after [2] alpha [3] cg its [4] relres
+// [5] nnz [6] trials.
+int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *prm,
+                const double *phi, const double *psi, double s, double *f, double *g,
+                EvalOut *cur, double *info, cudaStream_t st) {
+    const long long m = pb->m, n = pb->n, N = m + n;
+    const double tau = prm->theta / ((double)m * (double)n);
+    info[0] = cur->gnorm;
+    info[5] = (double)ws->nnz;
+    if (!ws->csr_ready) {
+        EvalOut e;
+        PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &e));
+        *cur = e;
+    }
+    PINS_TRY(build_csc(ws, m, n, ptr<long long>(ws->rowptr), ptr<int>(ws->colidx),
+                       ptr<double>(ws->val), ws->nnz, st));
+    double *rhs = ptr<double>(ws->rhs);
+    scale_concat_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(m, n, pb->eta, ptr<double>(ws->gradf),
+                                                              ptr<double>(ws->gradg), rhs);
+    PINS_CUDA(cudaGetLastError());
+    const double mu = prm->mu_rel * std::max(cur->maxr, cur->maxc);
+    const double rtol = cg_rtol(prm, cur->gnorm);
+    double *d = ptr<double>(ws->dir);
+    PINS_TRY(run_cg(ws, m, n, ptr<long long>(ws->rowptr), ptr<int>(ws->colidx), ptr<double>(ws->val),
+                    ptr<double>(ws->rowsum), ptr<double>(ws->colsum), mu, rhs, d, rtol,
+                    prm->cg_maxit, ptr<double>(ws->gradf), ptr<double>(ws->gradg), pb->a, pb->b, st));
+    PINS_CUDA(cudaMemcpyAsync(ws->h + 16, ws->cgst.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PINS_CUDA(cudaStreamSynchronize(st));
+    const double cg_its = ws->h[16], relres = ws->h[17], slope = ws->h[18], ad = ws->h[19];
+    info[3] = cg_its;
+    info[4] = relres;
+    double alpha = 1.0;
+    bool ok = false;
+    int trials = 0;
+    EvalOut e;
+    if (slope > 0.0 && std::isfinite(slope)) {
+        for (int t = 0; t < prm->max_backtracks; ++t) {
+            ++trials;
+            trial_prep_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(
+                m, n, alpha, 1.0 / pb->eta, f, g, d, ptr<double>(ws->ft), ptr<double>(ws->gt),
+                ptr<double>(ws->eu), ptr<double>(ws->ev));
+            PINS_CUDA(cudaGetLastError());
+            PINS_TRY(run_eval(ws, pb, phi, psi, s, ptr<double>(ws->ft), ptr<double>(ws->gt), tau, true,
+                              st, &e));
+            // P(x + alpha d) - P(x) = alpha <(a,b), d> + eta sum X_new expm1(-alpha(d_i+d_j)/eta)
+            const double inc = alpha * ad + pb->eta * e.em1;
+            if (std::isfinite(inc) && std::isfinite(e.gnorm) && inc >= prm->armijo_c * alpha * slope) {
+                ok = true;
+                break;
+            }
+            alpha *= prm->beta;
+        }
+    }
+    info[6] = trials;
+    if (ok) {
+        PINS_CUDA(cudaMemcpyAsync(f, ws->ft.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+        PINS_CUDA(cudaMemcpyAsync(g, ws->gt.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        *cur = e;
+        info[2] = alpha;
+    } else {
+        PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, cur));
+        info[2] = 0.0;
+    }
+    info[1] = cur->gnorm;
+    return PINS_OK;
+}
+
+int do_sweep(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi,
+             double s, double *f, double *g, cudaStream_t st) {
+    SweepArgs A;
+    A.m = pb->m;
+    A.n = pb->n;
+    A.cd = make_cd(pb);
+    A.phi = phi;
+    A.psi = psi;
+    A.a = pb->a;
+    A.b = pb->b;
+    A.f = f;
+    A.g = g;
+    A.eta = pb->eta;
+    A.inv_eta = 1.0 / pb->eta;
+    A.w = s * pb->cost_scale / pb->eta;
+    PINS_TRY(ensure(ws->tab, sizeof(ExpTable)));
+    A.tab = ptr<ExpTable>(ws->tab);
+    PINS_CUDA(launch_sweep(pb->cost_kind, pb->d, pb->m, pb->n, st, ws->nsm, A));
+    return PINS_OK;
+}
+
+bool outer_converged(const std::vector<double> &objs, const pins_params *p) {
+    const size_t k = objs.size();
+    if (k < 2) return false;
+    const double cur = objs.back();
+    const double scale = std::max(std::fabs(cur), 1e-300);
+    if (p->outer_rule == 0) return std::fabs(cur - objs[k - 2]) <= p->outer_tol * scale;
+    if (p->outer_rule == 1) {
+        const double half = objs[(k - 1) / 2];
+        return (half - cur) <= p->outer_tol * scale && k >= 4;
+    }
+    const size_t W = std::max<size_t>(5, k / 4);
+    if (k < 2 * W + 1) return false;
+    const double D1 = objs[k - 1 - 2 * W] - objs[k - 1 - W];
+    const double D2 = objs[k - 1 - W] - cur;
+    if (D2 <= 0.0) return D1 >= 0.0 && std::fabs(D2) <= p->outer_tol * scale;
+    if (D1 <= 0.0) return false;
+    const double r = D2 / D1;
+    if (r >= 1.0) return false;
+    return D2 * r / (1.0 - r) <= p->outer_tol * scale;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+extern "C" int pins_center_init(const pins_problem *pb, double *phi, double *psi, double *s_host,
+                                void *stream) {
+    PINS_TRY(check_problem(pb));
+    PINS_ARG(phi && psi && s_host, "phi, psi, s");
+    cudaStream_t st = (cudaStream_t)stream;
+    center_init_kernel<<<grid_1d(pb->m + pb->n, 148), 256, 0, st>>>(pb->m, pb->n, pb->eta, pb->a, pb->b,
+                                                                    phi, psi);
+    PINS_CUDA(cudaGetLastError());
+    *s_host = 1.0;
+    return PINS_OK;
+}
+
+extern "C" int pins_center_update(const pins_problem *pb, double *phi, double *psi, double *s_host,
+                                  const double *f, const double *g, void *stream) {
+    PINS_TRY(check_problem(pb));
+    PINS_ARG(phi && psi && s_host && f && g, "phi, psi, s, f, g");
+    cudaStream_t st = (cudaStream_t)stream;
+    center_update_kernel<<<grid_1d(pb->m + pb->n, 148), 256, 0, st>>>(pb->m, pb->n, pb->eta, f, g, phi,
+                                                                      psi);
+    PINS_CUDA(cudaGetLastError());
+    *s_host += 1.0;
+    return PINS_OK;
+}
+
+extern "C" int pins_sinkhorn_sweep(pins_workspace *ws, const pins_problem *pb, const double *phi,
+                                   const double *psi, double s, double *f, double *g, void *stream) {
+    PINS_ARG(ws != nullptr, "ws");
+    PINS_TRY(check_problem(pb));
+    PINS_ARG(phi && psi && f && g && s > 0.0, "phi, psi, f, g, s > 0");
+    return do_sweep(ws, pb, phi, psi, s, f, g, (cudaStream_t)stream);
+}
+
+extern "C" int pins_evaluate(pins_workspace *ws, const pins_problem *pb, const double *phi,
+                             const double *psi, double s, const double *f, const double *g, double tau,
+                             double *r, double *c, double *out_host, void *stream) {
+    PINS_ARG(ws != nullptr && out_host != nullptr, "ws, out_host");
+    PINS_TRY(check_problem(pb));
+    PINS_ARG(phi && psi && f && g && s > 0.0, "phi, psi, f, g, s > 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    EvalOut e;
+    PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &e));
+    if (r) PINS_CUDA(cudaMemcpyAsync(r, ws->rowsum.p, sizeof(double) * pb->m, cudaMemcpyDeviceToDevice, st));
+    if (c) PINS_CUDA(cudaMemcpyAsync(c, ws->colsum.p, sizeof(double) * pb->n, cudaMemcpyDeviceToDevice, st));
+    PINS_CUDA(cudaStreamSynchronize(st));
+    out_host[0] = e.gnorm;
+    out_host[1] = e.sumX;
+    out_host[2] = e.cost;
+    out_host[3] = e.dualP;
+    out_host[4] = tau > 0.0 ? (double)ws->nnz : 0.0;
+    out_host[5] = e.maxz;
+    return PINS_OK;
+}
+
+extern "C" int pins_get_csr(pins_workspace *ws, int64_t *rowptr, int32_t *colidx, double *val,
+                            int64_t cap, int64_t *nnz_host, int64_t *m_host) {
+    PINS_ARG(ws != nullptr && nnz_host && m_host, "pointers");
+    PINS_ARG(ws->csr_ready, "no CSR: call pins_evaluate with tau > 0 first");
+    PINS_CUDA(cudaDeviceSynchronize());
+    *nnz_host = ws->nnz;
+    *m_host = ws->m;
+    if (rowptr && colidx && val) {
+        PINS_ARG(cap >= ws->nnz, "cap < nnz");
+        PINS_CUDA(cudaMemcpy(rowptr, ws->rowptr.p, sizeof(int64_t) * (ws->m + 1), cudaMemcpyDeviceToDevice));
+        if (ws->nnz) {
+            PINS_CUDA(cudaMemcpy(colidx, ws->colidx.p, sizeof(int32_t) * ws->nnz, cudaMemcpyDeviceToDevice));
+            PINS_CUDA(cudaMemcpy(val, ws->val.p, sizeof(double) * ws->nnz, cudaMemcpyDeviceToDevice));
+        }
+    }
+    return PINS_OK;
+}
+
+extern "C" int pins_sparsify_dense(pins_workspace *ws, int64_t m, int64_t n, const double *P,
+                                   int64_t ldp, double tau, int64_t *rowptr, int32_t *colidx,
+                                   double *val, int64_t cap, int64_t *nnz_host, void *stream) {
+    PINS_ARG(ws && P && nnz_host && m >= 1 && n >= 1 && ldp >= n && tau > 0.0, "arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    PINS_TRY(ensure(ws->fsave, sizeof(double) * (m + n)));
+    PINS_TRY(ensure(ws->gsave, sizeof(double) * (m + n)));
+    PINS_CUDA(cudaMemsetAsync(ws->fsave.p, 0, sizeof(double) * (m + n), st));
+    PINS_CUDA(cudaMemsetAsync(ws->gsave.p, 0, sizeof(double) * (m + n), st));
+    // a dummy problem whose "cost" is the given plan (kernel KIND 3: X = P)
+    pins_problem pb;
+    memset(&pb, 0, sizeof pb);
+    pb.m = m; pb.n = n; pb.cost_kind = 3; pb.C = P; pb.ldc = ldp; pb.cost_scale = 1.0; pb.eta = 1.0;
+    pb.a = ptr<double>(ws->fsave); pb.b = ptr<double>(ws->fsave) + m;
+    const double *z = ptr<double>(ws->gsave);
+    EvalOut e;
+    PINS_TRY(run_eval(ws, &pb, z, z + m, 1.0, z, z + m, tau, false, st, &e));
+    int64_t mm = 0;
+    return pins_get_csr(ws, rowptr, colidx, val, cap, nnz_host, &mm);
+}
+
+extern "C" int pins_cg(pins_workspace *ws, int64_t m, int64_t n, const int64_t *rowptr,
+                       const int32_t *colidx, const double *val, int64_t nnz, const double *dr,
+                       const double *dc, double mu, const double *rhs, double *x, double rtol,
+                       int32_t maxit, int32_t *iters_host, double *relres_host, void *stream) {
+    PINS_ARG(ws && rowptr && dr && dc && rhs && x && iters_host && relres_host, "pointers");
+    PINS_ARG(m >= 1 && n >= 1 && nnz >= 0 && maxit >= 0, "sizes");
+    PINS_ARG(nnz == 0 || (colidx && val), "colidx/val");
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long *rp = reinterpret_cast<const long long *>(rowptr);
+    PINS_TRY(build_csc(ws, m, n, rp, colidx, val, nnz, st));
+    PINS_TRY(run_cg(ws, m, n, rp, colidx, val, dr, dc, mu, rhs, x, rtol, maxit, nullptr, nullptr,
+                    nullptr, nullptr, st));
+    PINS_CUDA(cudaMemcpyAsync(ws->h + 16, ws->cgst.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PINS_CUDA(cudaStreamSynchronize(st));
+    *iters_host = (int32_t)ws->h[16];
+    *relres_host = ws->h[17];
+    return PINS_OK;
+}
+
+extern "C" int pins_newton_step(pins_workspace *ws, const pins_problem *pb, const pins_params *prm,
+                                const double *phi, const double *psi, double s, double *f, double *g,
+                                double *info_host, void *stream) {
+    PINS_ARG(ws && prm && info_host, "ws, prm, info");
+    PINS_TRY(check_problem(pb));
+    PINS_ARG(phi && psi && f && g && s > 0.0, "phi, psi, f, g, s > 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    const double tau = prm->theta / ((double)pb->m * (double)pb->n);
+    EvalOut cur;
+    PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &cur));
+    return newton_iter(ws, pb, prm, phi, psi, s, f, g, &cur, info_host, st);
+}
+
+extern "C" int pins_residuals(pins_workspace *ws, const pins_problem *pb, const double *phi,
+                              const double *psi, double s, const double *f, const double *g, double *u,
+                              double *v, double *res_host, void *stream) {
+    PINS_ARG(ws && res_host, "ws, res");
+    PINS_TRY(check_problem(pb));
+    PINS_ARG(phi && psi && f && g && s > 0.0, "phi, psi, f, g, s > 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    EvalOut e;
+    PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, 0.0, false, st, &e));
+    const long long m = pb->m, n = pb->n;
+    PINS_TRY(prepare(ws, pb));
+    double *uu = u ? u : ptr<double>(ws->uv);
+    double *vv = v ? v : ptr<double>(ws->uv) + m;
+    lp_duals_kernel<<<grid_1d(m + n, ws->nsm), 256, 0, st>>>(m, n, pb->eta, 1.0 / s, f, g, phi, psi, uu, vv);
+    PINS_CUDA(cudaGetLastError());
+    dots_kernel<<<1, 1024, 0, st>>>(m, n, pb->a, uu, pb->b, vv, ptr<double>(ws->rowsum),
+                                    ptr<double>(ws->colsum), ptr<double>(ws->st));
+    PINS_CUDA(cudaMemcpyAsync(ws->h, ws->st.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PINS_CUDA(cudaStreamSynchronize(st));
+    res_host[0] = e.gnorm;
+    res_host[1] = std::max(0.0, pb->eta / s * e.maxz);
+    res_host[2] = e.cost;
+    res_host[3] = ws->h[8];
+    res_host[4] = e.cost - ws->h[8];
+    return PINS_OK;
+}
+
+extern "C" int pins_plan(const pins_problem *pb, const double *phi, const double *psi, double s,
+                         const double *f, const double *g, double *X, int64_t ldx, void *stream) {
+    PINS_TRY(check_problem(pb));
+    PINS_ARG(phi && psi && f && g && X && ldx >= pb->n && s > 0.0, "pointers / ldx");
+    cudaStream_t st = (cudaStream_t)stream;
+    // private exp table (same values as the workspace table)
+    static DevBuf tab;
+    if (!tab.p) {
+        ExpTable t;
+        for (int j = 0; j < 64; ++j) {
+            long double v = exp2l((long double)j / 64.0L);
+            t.hi[j] = (double)v;
+            t.lo[j] = (double)(v - (long double)t.hi[j]);
+        }
+        PINS_TRY(ensure(tab, sizeof(ExpTable)));
+        PINS_CUDA(cudaMemcpy(tab.p, &t, sizeof t, cudaMemcpyHostToDevice));
+    }
+    CostDesc cd = make_cd(pb);
+    const double inv_eta = 1.0 / pb->eta, w = s * pb->cost_scale / pb->eta;
+    const int G = grid_1d(pb->m * pb->n, 148, 16);
+    if (pb->cost_kind == 0)
+        plan_kernel<0, 0><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx);
+    else if (pb->cost_kind == 1)
+        plan_kernel<1, 16><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx);
+    else
+        plan_kernel<2, 16><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx);
+    PINS_CUDA(cudaGetLastError());
+    return PINS_OK;
+}
+
+extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream) {
+    PINS_TRY(check_problem(pb));
+    PINS_ARG(prm && res && res->f && res->g && res->phi && res->psi, "params / result buffers");
+    PINS_ARG(prm->K >= 1 && prm->T2 >= 0 && prm->T1 >= 0, "budgets");
+    auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t st = (cudaStream_t)stream;
+    pins_workspace *ws = nullptr;
+    PINS_TRY(pins_workspace_create(&ws));
+    struct Guard {
+        pins_workspace *w;
+        ~Guard() { pins_workspace_destroy(w); }
+    } guard{ws};
+    const long long m = pb->m, n = pb->n;
+    double *f = res->f, *g = res->g, *phi = res->phi, *psi = res->psi;
+    const double tau = prm->theta / ((double)m * (double)n);
+    double s = 1.0;
+    PINS_TRY(pins_center_init(pb, phi, psi, &s, stream));
+    PINS_CUDA(cudaMemsetAsync(f, 0, sizeof(double) * m, st));
+    PINS_CUDA(cudaMemsetAsync(g, 0, sizeof(double) * n, st));
+    std::vector<double> objs;
+    int sweeps = 0, newton_its = 0, cg_its = 0, k = 0;
+    bool converged = false;
+    EvalOut cur;
+    double s_last = s;
+    for (k = 0; k < prm->K; ++k) {
+        if (!prm->warm_start && k > 0) {
+            PINS_CUDA(cudaMemsetAsync(f, 0, sizeof(double) * m, st));
+            PINS_CUDA(cudaMemsetAsync(g, 0, sizeof(double) * n, st));
+        }
+        PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &cur));
+        int t = 0;
+        while (!(cur.gnorm <= prm->sink_tol) && t < prm->T1) {
+            PINS_TRY(do_sweep(ws, pb, phi, psi, s, f, g, st));
+            PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &cur));
+            ++t;
+        }
+        sweeps += t;
+        int tn = 0;
+        while (cur.gnorm > prm->newton_tol && tn < prm->T2) {
+            double info[8];
+            PINS_TRY(newton_iter(ws, pb, prm, phi, psi, s, f, g, &cur, info, st));
+            cg_its += (int)info[3];
+            ++tn;
+            if (info[2] == 0.0) break;
+        }
+        newton_its += tn;
+        if (res->obj_trace_host) res->obj_trace_host[k] = cur.cost;
+        objs.push_back(cur.cost);
+        res->obj = cur.cost;
+        res->kkt = cur.gnorm;
+        res->dual_obj = cur.dualP;
+        res->dual_inf = std::max(0.0, pb->eta / s * cur.maxz);
+        s_last = s;
+        // X^{k+1} = X~(f, g): centre update (Alg. 2 line 16), then C^{k+1} (line 3)
+        PINS_TRY(pins_center_update(pb, phi, psi, &s, f, g, stream));
+        if (outer_converged(objs, prm)) {
+            converged = true;
+            ++k;
+            break;
+        }
+    }
+    if (k > prm->K) k = prm->K;
+    // LP dual estimates of X^{K} (reading R8): u = phi/s_last, v = psi/s_last
+    // (phi, psi are already the updated centre; f, g folded in).
+    {
+        const double inv = 1.0 / s_last;
+        double *uu = res->u ? res->u : nullptr;
+        double *vv = res->v ? res->v : nullptr;
+        PINS_TRY(prepare(ws, pb));
+        if (!uu) uu = ptr<double>(ws->uv);
+        if (!vv) vv = ptr<double>(ws->uv) + m;
+        scale_concat_kernel<<<grid_1d(m + n, ws->nsm), 256, 0, st>>>(m, n, inv, phi, psi, ptr<double>(ws->dir));
+        PINS_CUDA(cudaMemcpyAsync(uu, ptr<double>(ws->dir), sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+        PINS_CUDA(cudaMemcpyAsync(vv, ptr<double>(ws->dir) + m, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        dots_kernel<<<1, 1024, 0, st>>>(m, n, pb->a, uu, pb->b, vv, ptr<double>(ws->rowsum),
+                                        ptr<double>(ws->colsum), ptr<double>(ws->st));
+        PINS_CUDA(cudaMemcpyAsync(ws->h, ws->st.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        PINS_CUDA(cudaStreamSynchronize(st));
+        res->lp_dual_obj = ws->h[8];
+        res->gap = res->obj - res->lp_dual_obj;
+    }
+    res->s = s;
+    res->outer_iters = k;
+    res->sweeps = sweeps;
+    res->newton_iters = newton_its;
+    res->cg_iters = cg_its;
+    res->status = converged ? 0 : 1;
+    res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return PINS_OK;
+}

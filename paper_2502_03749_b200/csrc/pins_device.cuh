@@ -1,0 +1,164 @@
+// pins_device.cuh -- device building blocks of the PINS hot path (sm_100a).
+//
+//  * pexp():   full-precision fp64 exp, table-driven (2^(j/64) hi/lo table in
+//              shared memory, degree-6 polynomial on |r| <= ln2/128).  ~10
+//              fp64 pipe ops instead of ~20 for the libdevice routine.
+//  * lse_push / lse_merge: online log-sum-exp state (max, scaled sum).
+//  * cost tiles: dense C rows (128-bit loads) or on-the-fly squared
+//              Euclidean / L1 distances from point coordinates.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pins {
+
+constexpr int kThreads = 256;          // 8 warps per CTA
+constexpr int kWarps = kThreads / 32;
+constexpr int kChunk = 2 * kThreads;   // columns per chunk (2 adjacent per thread)
+constexpr int kRMax = 32;              // max rows per CTA in the dense passes
+
+struct ExpTable {
+    double hi[64];
+    double lo[64];
+};
+
+// exp(z) for any z: 0 below -745.2 (with graceful denormals), +inf above 709.78,
+// NaN passthrough.  Max error ~1 ulp.
+__device__ __forceinline__ double pexp(double z, const double *__restrict__ thi,
+                                       const double *__restrict__ tlo) {
+    if (!(z > -745.2)) return (z != z) ? z : 0.0;
+    if (z > 709.78) return __longlong_as_double(0x7ff0000000000000LL);
+    const double kL2E64 = 92.332482616893657;                  // 64 / ln 2
+    const double kLn2Hi = 6.93147180369123816490e-01 * 0.015625;  // ln2_hi / 64 (21 trailing zero bits)
+    const double kLn2Lo = 1.90821492927058770002e-10 * 0.015625;  // ln2_lo / 64
+    const double kShift = 6755399441055744.0;                    // 1.5 * 2^52
+    double t = fma(z, kL2E64, kShift);
+    double kd = t - kShift;
+    int k = __double2loint(t);
+    double r = fma(-kd, kLn2Hi, z);
+    r = fma(-kd, kLn2Lo, r);
+    double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = p * r;                                                    // expm1(r)
+    int j = k & 63;
+    int e = k >> 6;
+    double th = thi[j];
+    double res = th + fma(th, p, tlo[j]);
+    if (e >= -1021) return res * __hiloint2double((e + 1023) << 20, 0);
+    return res * __hiloint2double((e + 1623) << 20, 0) * 0x1p-600;
+}
+
+__device__ __forceinline__ void load_exp_table(const ExpTable *__restrict__ g, double *shi,
+                                               double *slo) {
+    for (int t = threadIdx.x; t < 64; t += blockDim.x) {
+        shi[t] = g->hi[t];
+        slo[t] = g->lo[t];
+    }
+}
+
+// online log-sum-exp state: value = mx + log(sm)
+__device__ __forceinline__ void lse_push(double &mx, double &sm, double x, const double *thi,
+                                         const double *tlo) {
+    if (x > mx) {
+        sm = sm * pexp(mx - x, thi, tlo) + 1.0;
+        mx = x;
+    } else {
+        sm += pexp(x - mx, thi, tlo);
+    }
+}
+
+__device__ __forceinline__ void lse_merge(double &mx, double &sm, double mx2, double sm2,
+                                          const double *thi, const double *tlo) {
+    double M = fmax(mx, mx2);
+    if (M == -INFINITY) { mx = M; sm = 0.0; return; }
+    sm = sm * pexp(mx - M, thi, tlo) + sm2 * pexp(mx2 - M, thi, tlo);
+    mx = M;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ----------------------------------------------------------------- cost
+// Cost source shared by all dense passes.  D_ij is the unscaled distance;
+// callers fold cost_scale into their exponent weight.
+struct CostDesc {
+    int kind;          // 0 dense, 1 sqeuclid, 2 L1
+    int d;
+    const double *C;
+    long long ldc;
+    const double *x;   // m x d
+    const double *y;   // n x d
+    int vec2;          // dense: rows 16-byte aligned and ldc even -> 128-bit loads
+};
+
+// Per-thread column coordinates (2 adjacent columns j, j+1).
+template <int KIND, int DMAX>
+struct ColPts {
+    double y0[DMAX > 0 ? DMAX : 1];
+    double y1[DMAX > 0 ? DMAX : 1];
+    __device__ __forceinline__ void load(const CostDesc &cd, long long j, long long n) {
+        if constexpr (KIND == 1 || KIND == 2) {
+#pragma unroll
+            for (int k = 0; k < DMAX; ++k) {
+                y0[k] = (k < cd.d && j < n) ? cd.y[j * cd.d + k] : 0.0;
+                y1[k] = (k < cd.d && j + 1 < n) ? cd.y[(j + 1) * cd.d + k] : 0.0;
+            }
+        }
+    }
+};
+
+// distance of row point xr (shared memory, d values) to the two column points
+template <int KIND, int DMAX>
+__device__ __forceinline__ void pts_dist2(const double *__restrict__ xr, const ColPts<KIND, DMAX> &cp,
+                                          int d, double &D0, double &D1) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < DMAX; ++k) {
+        if (k < d) {
+            double xv = xr[k];
+            double t0 = xv - cp.y0[k];
+            double t1 = xv - cp.y1[k];
+            if constexpr (KIND == 1) {
+                s0 = fma(t0, t0, s0);
+                s1 = fma(t1, t1, s1);
+            } else {
+                s0 += fabs(t0);
+                s1 += fabs(t1);
+            }
+        }
+    }
+    D0 = s0;
+    D1 = s1;
+}
+
+// dense: the two entries C[i, j], C[i, j+1] (j even); tail-safe
+__device__ __forceinline__ void dense_load2(const CostDesc &cd, long long i, long long j, long long n,
+                                            double &D0, double &D1) {
+    const double *row = cd.C + i * cd.ldc;
+    if (cd.vec2 && j + 1 < n) {
+        double2 v = __ldg(reinterpret_cast<const double2 *>(row + j));
+        D0 = v.x;
+        D1 = v.y;
+    } else {
+        D0 = (j < n) ? __ldg(row + j) : 0.0;
+        D1 = (j + 1 < n) ? __ldg(row + j + 1) : 0.0;
+    }
+}
+
+}  // namespace pins

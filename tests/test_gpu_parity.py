@@ -1,0 +1,310 @@
+"""GPU parity: every hot-path call through the C ABI against the CPU oracle on
+the same seeded inputs (Eq. (7)-(9), Alg. 1/2, §3.2).
+
+Subproblem states (centre X^k and warm potentials) are produced by running
+the ORACLE's PINS for k outer iterations; the GPU receives the centre in its
+factored log form (phi, psi, s), the oracle keeps its dense C^k = C - eta log X^k.
+Agreement therefore also checks the factorisation identity of DESIGN.md §2.
+
+Tolerances (derived in DESIGN.md §6): plan entries and sums are fp64 with
+exponents of magnitude |z| <= s max C / eta, so relative errors are bounded by
+~1e-16 * |z|; we allow 1e-11 relative (+ small absolute floors).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import pins_oracle as po  # noqa: E402
+from oracle.exact_lp import solve_exact  # noqa: E402
+from workloads import make  # noqa: E402
+from workloads.gen import COST_DENSE, Workload  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2502_03749_b200 import build as b
+    b.build()
+    from paper_2502_03749_b200 import pins
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return pins
+
+
+def T(x):
+    return torch.as_tensor(np.asarray(x), dtype=torch.float64, device="cuda").contiguous()
+
+
+def H(t):
+    return t.detach().cpu().numpy()
+
+
+def ragged(m, n, seed, kind="dense", d=3):
+    """Ragged-size instance (not multiples of the 512-column chunk / 32-row tile)."""
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(0.1, 1, m); a /= a.sum()
+    b = rng.uniform(0.1, 1, n); b /= b.sum()
+    if kind == "dense":
+        return Workload("ragged", m, n, COST_DENSE, a, b, 0.05, C=rng.random((m, n)))
+    X = np.floor(rng.random((m, d)) * 1024); Y = np.floor(rng.random((n, d)) * 1024)
+    from workloads.gen import _points_workload, COST_SQEUCLID, COST_L1
+    return _points_workload("ragged_pts", X, Y, COST_SQEUCLID if kind == "sq" else COST_L1, a, b, 0.05)
+
+
+CASES = [
+    ("c0", lambda: make("c0_pts64")),
+    ("c1s", lambda: make("c1_rand1k", scale=0.11)),
+    ("c2s", lambda: make("c2_img4k", scale=0.06)),
+    ("c3s", lambda: make("c3_gmm10k", scale=0.013)),
+    ("c4s", lambda: make("c4_l1rect", scale=0.012)),
+    ("rag_dense", lambda: ragged(37, 1029, 5)),
+    ("rag_sq", lambda: ragged(70, 515, 6, "sq", 10)),
+    ("rag_l1", lambda: ragged(33, 17, 7, "l1", 3)),
+]
+
+
+def oracle_state(w, k, **kw):
+    """Oracle PINS after k outer iterations: (C, C^k dense, phi, psi, s, f, g)."""
+    C = po.cost_matrix(w)
+    prm = po.Params(eta=w.eta, K=k, outer_tol=0.0, newton_tol=1e-10, **kw)
+    r = po.pins(C, w.a, w.b, prm)
+    Ck = po.shifted_cost(C, r.logX, w.eta)
+    return C, Ck, r.phi, r.psi, r.s_next, r.f, r.g
+
+
+@pytest.mark.parametrize("name,mk", CASES)
+@pytest.mark.parametrize("k", [0, 3])
+def test_plan_and_evaluate(P, name, mk, k):
+    w = mk()
+    if k == 0:
+        C = po.cost_matrix(w)
+        Ck = po.shifted_cost(C, np.log(w.a)[:, None] + np.log(w.b)[None, :], w.eta)
+        phi, psi, s = w.eta * np.log(w.a), w.eta * np.log(w.b), 1.0
+        rng = np.random.default_rng(1)
+        f, g = rng.normal(0, 0.3 * w.eta, w.m), rng.normal(0, 0.3 * w.eta, w.n)
+    else:
+        C, Ck, phi, psi, s, f, g = oracle_state(w, k)
+    pb = P.DeviceProblem.from_workload(w)
+    X = H(P.plan(pb, T(phi), T(psi), s, T(f), T(g)))
+    Xo = po.plan(f, g, Ck, w.eta)
+    scale = max(1.0, s * C.max() / w.eta)
+    np.testing.assert_allclose(X, Xo, rtol=4e-15 * scale, atol=1e-300)
+    ws = P.Workspace()
+    ev = P.evaluate(ws, pb, T(phi), T(psi), s, T(f), T(g))
+    gf, gg = po.dual_gradient(f, g, Ck, w.a, w.b, w.eta)
+    np.testing.assert_allclose(H(ev["r"]), Xo.sum(1), rtol=4e-15 * scale, atol=1e-300)
+    np.testing.assert_allclose(H(ev["c"]), Xo.sum(0), rtol=4e-15 * scale, atol=1e-300)
+    gn = np.abs(gf).sum() + np.abs(gg).sum()
+    assert abs(ev["grad_l1"] - gn) <= 1e-14 * scale * (1 + gn)
+    assert abs(ev["sum_x"] - Xo.sum()) <= 1e-14 * scale * Xo.sum()
+    assert abs(ev["cost"] - (C * Xo).sum()) <= 1e-13 * scale * abs((C * Xo).sum()) + 1e-300
+    Po = po.dual_objective(f, g, Ck, w.a, w.b, w.eta)
+    # P^k itself is large relative to its changes; compare in the scale of its terms
+    assert abs(ev["dual_obj"] - Po) <= 1e-13 * (abs(w.a @ f) + abs(w.b @ g) + w.eta * Xo.sum() + 1)
+
+
+@pytest.mark.parametrize("name,mk", CASES)
+def test_sparsify_pattern_in_eval_matches_threshold(P, name, mk):
+    w = mk()
+    C, Ck, phi, psi, s, f, g = oracle_state(w, 2)
+    pb = P.DeviceProblem.from_workload(w)
+    tau = 1e-4 / (w.m * w.n)
+    ws = P.Workspace()
+    ev = P.evaluate(ws, pb, T(phi), T(psi), s, T(f), T(g), tau=tau)
+    rp, ci, va = (H(t) for t in P.get_csr(ws))
+    Xo = po.plan(f, g, Ck, w.eta)
+    mask_o = po.sparsify_threshold(Xo, tau)
+    rows = np.repeat(np.arange(w.m), np.diff(rp))
+    mask_g = np.zeros_like(mask_o)
+    mask_g[rows, ci] = True
+    # columns ascending inside every row
+    for i in range(w.m):
+        seg = ci[rp[i]:rp[i + 1]]
+        assert np.all(np.diff(seg) > 0)
+    # identical except entries within rounding of tau
+    near = np.abs(Xo - tau) <= 1e-11 * tau
+    assert np.array_equal(mask_o & ~near, mask_g & ~near)
+    assert ev["nnz"] == len(ci)
+    np.testing.assert_allclose(va, Xo[rows, ci], rtol=1e-11)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 700), (64, 64), (37, 1029), (300, 5)])
+def test_sparsify_dense_bit_exact(P, shape):
+    # identical P on both sides: the CSR pattern must match bit for bit,
+    # including entries exactly equal to tau (kept: P >= tau).
+    m, n = shape
+    rng = np.random.default_rng(m * 1000 + n)
+    Pm = rng.random((m, n)) ** 4
+    tau = 0.3
+    Pm[rng.random((m, n)) < 0.05] = tau
+    ws = P.Workspace()
+    rp, ci, va = (H(t) for t in P.sparsify_dense(ws, T(Pm), tau))
+    rpo, cio, vao = po.csr_from_mask(Pm, po.sparsify_threshold(Pm, tau))
+    assert np.array_equal(rp, rpo) and np.array_equal(ci, cio) and np.array_equal(va, vao)
+
+
+@pytest.mark.parametrize("name,mk", CASES)
+@pytest.mark.parametrize("k", [0, 2])
+def test_sinkhorn_sweep(P, name, mk, k):
+    w = mk()
+    if k == 0:
+        C = po.cost_matrix(w)
+        Ck = po.shifted_cost(C, np.log(w.a)[:, None] + np.log(w.b)[None, :], w.eta)
+        phi, psi, s = w.eta * np.log(w.a), w.eta * np.log(w.b), 1.0
+        f, g = np.zeros(w.m), np.zeros(w.n)
+    else:
+        C, Ck, phi, psi, s, f, g = oracle_state(w, k)
+    pb = P.DeviceProblem.from_workload(w)
+    ws = P.Workspace()
+    fd, gd = T(f), T(g)
+    for _ in range(3):
+        P.sinkhorn_sweep(ws, pb, T(phi), T(psi), s, fd, gd)
+        f, g = po.sinkhorn_sweep(f, g, Ck, w.a, w.b, w.eta)
+    scale = max(1.0, s * C.max() / w.eta)
+    tol = 1e-14 * scale * w.eta * 10
+    np.testing.assert_allclose(H(fd), f, rtol=0, atol=tol * (1 + np.abs(f).max() / w.eta))
+    np.testing.assert_allclose(H(gd), g, rtol=0, atol=tol * (1 + np.abs(g).max() / w.eta))
+
+
+def test_cg_against_direct_solve(P):
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    w = make("c1_rand1k", scale=0.1)
+    C, Ck, phi, psi, s, f, g = oracle_state(w, 2)
+    Xo = po.plan(f, g, Ck, w.eta)
+    tau = 1e-4 / (w.m * w.n)
+    rp, ci, va = po.csr_from_mask(Xo, po.sparsify_threshold(Xo, tau))
+    r, c = Xo.sum(1), Xo.sum(0)
+    m, n = w.m, w.n
+    mu = 1e-8
+    Xs = sp.csr_matrix((va, ci, rp), shape=(m, n))
+    M = sp.bmat([[sp.diags(r), Xs], [Xs.T, sp.diags(c)]]).tocsc() + mu * sp.eye(m + n)
+    rhs = np.random.default_rng(3).normal(size=m + n)
+    x_ref = spla.spsolve(M, rhs)
+    ws = P.Workspace()
+    x, its, rel = P.cg(ws, m, n, torch.as_tensor(rp, device="cuda"), torch.as_tensor(ci.astype(np.int32), device="cuda"),
+                       T(va), T(r), T(c), mu, T(rhs), rtol=1e-12, maxit=20000)
+    assert rel <= 1e-12
+    res = np.linalg.norm(M @ H(x) - rhs) / np.linalg.norm(rhs)
+    # true residual vs the recursive one: q = M z + beta q drifts by O(its * eps * cond)
+    assert res <= 1e-10
+    # oracle CG (same algorithm, same preconditioner) reaches the same solution
+    xo, _, _ = po.cg(lambda p: M @ p, rhs, 1e-12, 20000, diag=np.concatenate([r, c]) + mu)
+    np.testing.assert_allclose(H(x), xo, rtol=1e-6, atol=1e-9 * np.abs(xo).max())
+    np.testing.assert_allclose(H(x), x_ref, rtol=1e-6, atol=1e-9 * np.abs(x_ref).max())
+
+
+@pytest.mark.parametrize("name,mk", CASES[:5])
+def test_newton_step(P, name, mk):
+    w = mk()
+    C, Ck, phi, psi, s, f, g = oracle_state(w, 2)
+    # start away from the subproblem optimum: one plain sweep from the warm start
+    prm_o = po.Params(eta=w.eta, cg_tol=1e-12, cg_forcing=0.0, cg_maxit=5000)
+    prm_g = P.default_params(cg_tol=1e-12, cg_forcing=0.0, cg_maxit=5000)
+    pb = P.DeviceProblem.from_workload(w)
+    ws = P.Workspace()
+    fd, gd = T(f), T(g)
+    for _ in range(2):
+        info = P.newton_step(ws, pb, prm_g, T(phi), T(psi), s, fd, gd)
+        f2, g2, io = po.newton_step(f, g, Ck, w.a, w.b, w.eta, prm_o)
+        assert info["alpha"] == io["alpha"]
+        assert info["nnz"] == io["nnz"] or abs(info["nnz"] - io["nnz"]) <= 2
+        dnorm = np.abs(f2 - f).max() + np.abs(g2 - g).max()
+        np.testing.assert_allclose(H(fd), f2, rtol=0, atol=1e-7 * dnorm + 1e-13)
+        np.testing.assert_allclose(H(gd), g2, rtol=0, atol=1e-7 * dnorm + 1e-13)
+        res_o = po.residual_l1(f2, g2, Ck, w.a, w.b, w.eta)
+        assert abs(info["grad_after"] - res_o) <= 1e-6 * info["grad_before"] + 1e-13
+        f, g = f2, g2
+
+
+def test_center_update_and_residuals(P):
+    w = make("c1_rand1k", scale=0.08)
+    C, Ck, phi, psi, s, f, g = oracle_state(w, 3)
+    pb = P.DeviceProblem.from_workload(w)
+    ph, ps = T(phi), T(psi)
+    s2 = P.center_update(pb, ph, ps, s, T(f), T(g))
+    assert s2 == s + 1
+    # X^{k+1} = X~(f, g) (Alg. 2 line 16) and C^{k+1} = C - eta log X^{k+1} (line 3)
+    logX = po.log_plan(f, g, Ck, w.eta)
+    Ck1 = po.shifted_cost(C, logX, w.eta)
+    Ck1_gpu = s2 * C - H(ph)[:, None] - H(ps)[None, :]
+    np.testing.assert_allclose(Ck1_gpu, Ck1, rtol=0, atol=1e-13 * s2 * C.max())
+    ws = P.Workspace()
+    rr = P.residuals(ws, pb, T(phi), T(psi), s, T(f), T(g))
+    u, v = (f + phi) / s, (g + psi - w.eta) / s
+    ko = po.kkt(C, logX, w.a, w.b, u, v)
+    np.testing.assert_allclose(H(rr["u"]), u, rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(H(rr["v"]), v, rtol=1e-14, atol=1e-15)
+    assert abs(rr["kkt"] - ko["primal"]) <= 1e-12
+    assert abs(rr["obj"] - ko["pobj"]) <= 1e-13
+    assert abs(rr["lp_dual_obj"] - ko["dobj"]) <= 1e-13
+    assert abs(rr["dual_inf"] - ko["dual_inf"]) <= 1e-12
+
+
+def test_solve_matches_oracle_fixed_iterations(P):
+    w = make("c1_rand1k", scale=0.1)
+    C = po.cost_matrix(w)
+    K = 25
+    o = po.pins(C, w.a, w.b, po.Params(eta=w.eta, K=K, outer_tol=0.0, newton_tol=1e-11), trace=True)
+    pb = P.DeviceProblem.from_workload(w)
+    prm = P.default_params(K=K, outer_tol=0.0, newton_tol=1e-11)
+    r = P.solve(pb, prm, trace=True)
+    assert r["outer_iters"] == K
+    to = np.array([t["obj"] for t in o.trace])
+    np.testing.assert_allclose(np.array(r["trace"]), to, rtol=1e-9)
+    assert r["kkt"] <= 1e-11 and o.kkt["primal"] <= 1e-11
+    np.testing.assert_allclose(H(r["u"]), o.u, rtol=0, atol=1e-9)
+    np.testing.assert_allclose(H(r["v"]), o.v, rtol=0, atol=1e-9)
+
+
+BENCH = dict(K=20000, outer_rule=1, outer_tol=1e-7, newton_tol=1e-10)
+
+
+@pytest.mark.parametrize("name", ["c0_pts64"])
+def test_solve_full_size_reaches_exact_lp(P, name):
+    gold = json.load(open(os.path.join(GOLD, f"exact_{name}.json")))
+    w = make(name)
+    pb = P.DeviceProblem.from_workload(w)
+    r = P.solve(pb, P.default_params(**BENCH))
+    assert r["kkt"] <= 1e-8
+    assert abs(r["obj"] - gold["obj"]) <= 1e-7 * abs(gold["obj"])
+
+
+@pytest.mark.parametrize("name,scale", [("c1_rand1k", 0.125), ("c2_img4k", 0.06), ("c4_l1rect", 0.01),
+                                        ("c3_gmm10k", 0.01)])
+def test_solve_small_scale_reaches_exact_lp(P, name, scale):
+    w = make(name, scale=scale)
+    ex = solve_exact(po.cost_matrix(w), w.a, w.b)
+    pb = P.DeviceProblem.from_workload(w)
+    r = P.solve(pb, P.default_params(**BENCH), trace=True)
+    assert r["kkt"] <= 1e-8
+    assert abs(r["obj"] - ex["obj"]) <= 1e-7 * abs(ex["obj"])
+    tr = np.array(r["trace"])
+    # Thm 4.1: <C, X^{k+1}> <= <C, X^k> (inexact solves: 1e-10 slack)
+    assert np.all(np.diff(tr) <= 1e-10 * abs(tr[0]))
+
+
+def test_edge_cases(P):
+    # single cell: the only feasible plan is [[1]]
+    w = Workload("one", 1, 1, COST_DENSE, np.ones(1), np.ones(1), 0.01, C=np.array([[0.3]]))
+    r = P.solve(P.DeviceProblem.from_workload(w), P.default_params(K=5))
+    assert abs(r["obj"] - 0.3) <= 1e-12 and r["kkt"] <= 1e-12
+    # single row / column: plan is forced (a b^T)
+    rng = np.random.default_rng(0)
+    b = rng.random(300) + 0.1; b /= b.sum()
+    w = Workload("row", 1, 300, COST_DENSE, np.ones(1), b, 0.01, C=rng.random((1, 300)))
+    r = P.solve(P.DeviceProblem.from_workload(w), P.default_params(K=5))
+    assert abs(r["obj"] - (w.C[0] @ b)) <= 1e-10 and r["kkt"] <= 1e-8
+    # invalid arguments fail loudly (no fallback)
+    bad = P.DeviceProblem(0, 4, 0, T(np.ones(1)), T(np.ones(4) / 4), 0.1, C=T(np.zeros((1, 4))))
+    with pytest.raises(RuntimeError):
+        P.solve(bad)
+    bad = P.DeviceProblem(2, 2, 0, T(np.ones(2) / 2), T(np.ones(2) / 2), -1.0, C=T(np.zeros((2, 2))))
+    with pytest.raises(RuntimeError):
+        P.solve(bad)
