@@ -1,0 +1,359 @@
+"""bench.py -- PINS on B200: seconds to KKT <= 1e-8 on BASELINE.json's n=10k config.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3_gmm10k] [--no-cpu-baseline]
+
+A *step* is one complete pins_solve (Algorithm 2 of PAPER.md: every EPPA outer
+iteration with its Sinkhorn sweeps, sparse-Newton/CG steps, line searches and
+proximal-centre updates) on the seeded synthetic workload `--config`
+(default c3_gmm10k: m = n = 10000 points of an 8-component Gaussian mixture in
+R^10, squared-Euclidean cost recomputed on the fly, eta = 1e-3).
+Inputs are resident in HBM when the timed region starts.  Each step must reach
+KKT residual <= 1e-8 and match the exact LP optimum (tests/golden, written by
+the oracle's network simplex) to 1e-7 relative, else the run fails.
+
+value  = max-over-ranks device time of the K timed steps / (K * N): seconds
+         per solve at whole-job throughput (N ranks solve independent copies:
+         replicas, no collective on the data path, "scaling": "weak").
+e2e    = the same through pins_solve_host: instance copied from pinned host
+         memory and the LP duals (u, v) copied back inside the timed region.
+roofline = dominant kernel class from the library's own event profile
+         (pins_prof_*, CUDA events on the launching stream) over the timed
+         region; its bound and algorithmic work per launch are in DESIGN.md §7.
+cpu_baseline = the fp64 oracle (oracle/pins_oracle.py) as it stands, timed on
+         a bounded sample of the same instance (per-operation times of one
+         Sinkhorn sweep, one residual evaluation and one Newton step at full
+         size), scaled by this run's operation counts to seconds per solve.
+
+`--impl reference` runs only that oracle leg (rank 0; other ranks exit 0) and
+prints the same JSON line with "impl": "reference"; its operation counts come
+from the committed work profile profiles/workprofile_<config>.json (written by
+this script's own arm from a measured GPU solve).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BENCH_PARAMS = dict(K=20000, outer_rule=1, outer_tol=1e-7, newton_tol=1e-10)
+KKT_TARGET = 1e-8
+OBJ_RTOL = 1e-7
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3_gmm10k")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of oracle work for cpu_baseline")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ work model
+def algorithmic_work(cls: str, w) -> dict:
+    """Algorithmic work of ONE launch of a dense-pass kernel class.
+
+    Dense passes touch every (i, j) of the m x n block once.  For point costs
+    there is no m x n operand in HBM (the cost is recomputed from the m + n
+    points), so the pass is bound by the fp64 pipe: the exponential of
+    Eq. (7) per entry.  For a dense cost the operand C is read once per pass
+    (8 bytes per entry): HBM bound."""
+    mn = float(w.m) * float(w.n)
+    if w.kind == 0:
+        return {"bound": "hbm", "unit": "GB/s", "per_launch": 8.0 * mn, "what": "8 B of C per entry"}
+    return {"bound": "alu", "unit": "Gexp/s", "per_launch": mn, "what": "one fp64 exp (Eq. (7)) per entry"}
+
+
+def alu_peak_gexp(sm_mhz: float) -> float:
+    """fp64-pipe roofline of the point-cost dense passes, in entries (exps) per second.
+
+    B200: 148 SMs x 64 fp64 lanes per clock.  The minimal fp64 work of one entry
+    of a sweep / eval pass is FP64_OPS_PER_ENTRY pipe operations (exp: range
+    reduction 3, degree-6 polynomial 6, reconstruction 2; the exponent
+    z = R + S - w D: 1; the accumulation: 1).  Peak = lanes*clock / ops."""
+    FP64_OPS_PER_ENTRY = 13.0
+    return 148 * 64 * sm_mhz * 1e6 / FP64_OPS_PER_ENTRY / 1e9
+
+
+# ------------------------------------------------------------ cpu baseline
+def oracle_rates(w, budget_s: float):
+    """Time the oracle's own operations on the FULL instance (bounded: one call
+    each, stops early when the budget is spent).  Returns seconds per op."""
+    import numpy as np
+    from oracle import pins_oracle as po
+    t0 = time.time()
+    C = po.cost_matrix(w)
+    t_cost = time.time() - t0
+    logX0 = np.log(w.a)[:, None] + np.log(w.b)[None, :]
+    Ck = po.shifted_cost(C, logX0, w.eta)
+    f = np.zeros(w.m)
+    g = np.zeros(w.n)
+    t0 = time.time()
+    f, g = po.sinkhorn_sweep(f, g, Ck, w.a, w.b, w.eta)
+    t_sweep = time.time() - t0
+    t0 = time.time()
+    po.residual_l1(f, g, Ck, w.a, w.b, w.eta)
+    t_eval = time.time() - t0
+    t_newton = None
+    spent = t_cost + t_sweep + t_eval
+    if spent + 4 * t_eval < budget_s:
+        prm = po.Params(eta=w.eta)
+        t0 = time.time()
+        po.newton_step(f, g, Ck, w.a, w.b, w.eta, prm)
+        t_newton = time.time() - t0
+    if t_newton is None:
+        t_newton = 4 * t_eval      # plan + sparsify + one line-search trial, lower bound
+    return dict(sweep=t_sweep, eval=t_eval, newton=t_newton, cost=t_cost)
+
+
+def cpu_baseline(w, counts: dict, budget_s: float, cores: int):
+    r = oracle_rates(w, budget_s)
+    outer, sweeps, newton = counts["outer_iters"], counts["sweeps"], counts["newton_iters"]
+    # oracle PINS per outer iteration: one shifted cost + one residual, per sweep a
+    # sweep + a residual, per Newton step a step + a residual, plus the centre update
+    est = (outer * (r["cost"] * 0 + r["eval"] * 2) + sweeps * (r["sweep"] + r["eval"])
+           + newton * (r["newton"] + r["eval"]))
+    sample = (f"oracle fp64 numpy on the full {w.m}x{w.n} instance: one Sinkhorn sweep "
+              f"{r['sweep']:.2f}s, one residual {r['eval']:.2f}s, one Newton step {r['newton']:.2f}s, "
+              f"scaled by {outer} outer / {sweeps} sweeps / {newton} Newton steps per solve")
+    return {"value": est, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample}
+
+
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info()]
+        return max(n) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ main
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from workloads import make
+    w = make(args.config)
+    prof_path = os.path.join(ROOT, "profiles", f"workprofile_{args.config}.json")
+    if not os.path.exists(prof_path):
+        print(json.dumps({"impl": "reference", "unavailable": f"no work profile {prof_path}"}))
+        return
+    counts = json.load(open(prof_path))["counts"]
+    cores = blas_threads()
+    vals = []
+    for _ in range(args.warmup):
+        pass   # the oracle has no warm state; warm-up steps are not repeated
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(w, counts, args.cpu_budget, cores))
+    v = statistics.median([x["value"] for x in vals])
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {"impl": "reference", "metric": "s to KKT<1e-8 (n=10k, c3_gmm10k)", "value": v, "unit": "s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "m": w.m, "n": w.n, "eta": w.eta},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2502_03749_b200 import pins
+    from workloads import make
+
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = make(args.config)
+    gold_path = os.path.join(ROOT, "tests", "golden", f"exact_{args.config}.json")
+    gold = json.load(open(gold_path))["obj"] if os.path.exists(gold_path) else None
+    pb = pins.DeviceProblem.from_workload(w)
+    prm = pins.default_params(**BENCH_PARAMS)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # 512 MB > 126 MB L2
+
+    def check(r):
+        ok = r["kkt"] <= KKT_TARGET and (gold is None or abs(r["obj"] - gold) <= OBJ_RTOL * abs(gold))
+        if not ok:
+            raise SystemExit(f"bench step failed the accuracy bar: kkt {r['kkt']:.3e} obj {r['obj']!r} "
+                             f"exact {gold!r}")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        check(pins.solve(pb, prm))
+    # ---- timed region (device) ----
+    sampler = ClockSampler(local)
+    sampler.start()
+    pins.prof_reset()
+    pins.prof_enable(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    results = []
+    barrier()
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        r = pins.solve(pb, prm, want_duals=False)
+        ev[k][1].record(stream)
+        results.append(r)
+    barrier()
+    pins.prof_enable(False)
+    prof = pins.prof_read()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    for r in results:
+        check(r)
+    tot_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
+    T = tot_ms.item() / 1e3
+    value = T / (args.steps * world)
+
+    # ---- end to end through the host-buffer C-ABI call ----
+    hp = pins.HostProblem(w)
+    pins.solve_host(hp, prm)
+    barrier()
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    io = None
+    for k in range(args.steps):
+        flush.zero_()
+        e2e_ev[k][0].record(stream)
+        r = pins.solve_host(hp, prm)
+        e2e_ev[k][1].record(stream)
+        check(r)
+        io = (r["h2d_bytes"], r["d2h_bytes"])
+    barrier()
+    e2e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in e2e_ev)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = e2e_ms.item() / 1e3 / (args.steps * world)
+
+    if rank == 0:
+        r0 = results[-1]
+        counts = {k: r0[k] for k in ("outer_iters", "sweeps", "newton_iters", "cg_iters")}
+        dense = {c: prof[c] for c in ("sweep_row", "sweep_col", "eval")}
+        dom = max(dense, key=lambda c: dense[c]["ms"])
+        total_ms = sum(v["ms"] for v in prof.values())
+        L = max(1, dense[dom]["launches"])
+        avg_ms = dense[dom]["ms"] / L
+        wk = algorithmic_work(dom, w)
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        if wk["bound"] == "hbm":
+            achieved = wk["per_launch"] / (avg_ms * 1e-3) / 1e9
+            peak = peaks.get("hbm_gbs", 6650.0)
+            peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+        else:
+            achieved = wk["per_launch"] / (avg_ms * 1e-3) / 1e9
+            peak = alu_peak_gexp(clocks["sm_mhz"] or 1965.0)
+            peak_src = "derived: 148 SM x 64 fp64 lanes x sm clock / 13 fp64 ops per entry (DESIGN.md §7)"
+        roof = {"bound": wk["bound"], "kernel": dom, "achieved": achieved, "peak": peak, "unit": wk["unit"],
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "launches": dense[dom]["launches"], "avg_launch_us": avg_ms * 1e3,
+                "share_of_device_time": dense[dom]["ms"] / max(total_ms, 1e-9), "work": wk["what"]}
+        launches = int(sum(v["launches"] for v in prof.values()))
+        line = {
+            "metric": "s to KKT<1e-8 (n=10k, c3_gmm10k)", "value": value, "unit": "s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": T * 1e3 / args.steps, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "m": w.m, "n": w.n, "eta": w.eta,
+                       "cost": ["dense", "sqeuclid", "l1"][w.kind], "params": BENCH_PARAMS,
+                       "l2": "flushed (512 MB write) before every timed step",
+                       "parallelism": f"replicas x{world}"},
+            "accuracy": {"kkt": r0["kkt"], "obj": r0["obj"], "exact_obj": gold,
+                         "rel_err": None if gold is None else abs(r0["obj"] - gold) / abs(gold),
+                         "dual_inf": r0["dual_inf"], "gap": r0["gap"]},
+            "counts": counts,
+            "clocks": clocks,
+            "roofline": roof,
+            "prof": {c: {"launches": v["launches"], "ms_per_step": v["ms"] / args.steps} for c, v in prof.items()},
+            "gpu_launches": launches,
+            "e2e": {"value": e2e_value, "unit": "s", "h2d_bytes_per_step": io[0], "d2h_bytes_per_step": io[1]},
+        }
+        os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(w, counts, args.cpu_budget, blas_threads())
+        # the work profile the reference arm scales by (counts of this measured solve)
+        with open(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "profiles",
+                               f"workprofile_{args.config}.json"), "w") as fh:
+            json.dump({"config": args.config, "counts": counts, "source": "bench.py GPU solve"}, fh)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

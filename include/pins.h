@@ -188,6 +188,38 @@ typedef struct pins_result {
 /* Full PINS solve, Algorithm 2.  Synchronises.            */
 int pins_solve(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream);
 
+/* End-to-end solve from HOST memory (bench.py's e2e leg): pb_host is a
+ * pins_problem whose C / x / y / a / b point to HOST memory (pinned for the
+ * asynchronous path; pageable works but synchronises).  The instance is
+ * copied host->device on `stream` into library-owned stream-ordered device
+ * memory, pins_solve runs, and the outputs requested in res_host (f, g, phi,
+ * psi, u, v: HOST pointers, each may be NULL) are copied device->host.
+ * io_bytes_host[0] / [1] receive the host->device / device->host byte counts.
+ * Device memory is released before return.  Synchronises.                    */
+int pins_solve_host(const pins_problem *pb_host, const pins_params *prm, pins_result *res_host,
+                    int64_t *io_bytes_host, void *stream);
+
+/* ------------------------------------------------------------------ profiling
+ * Device-time profile of this library's own kernel launches (used by bench.py
+ * for the roofline of the dominant kernel).  Every launch is counted per
+ * class; while enabled, each launch is bracketed by a pair of CUDA events on
+ * the stream it is launched on (adds ~2 event records per launch).
+ * pins_prof_read synchronises on the pending events and returns, for a class,
+ * the number of launches and the summed device milliseconds since the last
+ * pins_prof_reset.  Process-global, not thread-safe.                          */
+#define PINS_PROF_SWEEP_ROW 0   /* Sinkhorn row pass (f update)                */
+#define PINS_PROF_SWEEP_COL 1   /* Sinkhorn column pass (g update)             */
+#define PINS_PROF_EVAL 2        /* plan evaluation / sparsify / trial pass     */
+#define PINS_PROF_REDUCE 3      /* column-partial and scalar reductions        */
+#define PINS_PROF_CSR 4         /* CSR / CSC construction                      */
+#define PINS_PROF_CG 5          /* conjugate gradient                          */
+#define PINS_PROF_VEC 6         /* small vector kernels                        */
+#define PINS_PROF_PLAN 7        /* dense plan materialisation                  */
+#define PINS_PROF_NCLASS 8
+void pins_prof_enable(int32_t on);
+void pins_prof_reset(void);
+int pins_prof_read(int32_t cls, int64_t *launches, double *ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -38,6 +39,73 @@ extern "C" const char *pins_last_error(void) { return g_err; }
             return PINS_ERR_ARG;                                         \
         }                                                                \
     } while (0)
+
+
+// ---------------------------------------------------------------- profiling
+// Device-time profile of this library's own launches (pins_prof_*, include/pins.h).
+// Every launch is counted; when enabled, a pair of CUDA events brackets it on
+// its own stream and pins_prof_read() folds the elapsed times per class.
+namespace {
+struct Prof {
+    bool on = false;
+    long long launches[PINS_PROF_NCLASS] = {};
+    double ms[PINS_PROF_NCLASS] = {};
+    std::vector<cudaEvent_t> pool;
+    struct Pend { int cls; cudaEvent_t a, b; };
+    std::vector<Pend> pend;
+    cudaEvent_t get() {
+        if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
+    void fold() {
+        for (auto &p : pend) {
+            float t = 0.f;
+            if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess)
+                ms[p.cls] += t;
+            pool.push_back(p.a);
+            pool.push_back(p.b);
+        }
+        pend.clear();
+    }
+};
+Prof g_prof;
+struct ProfScope {
+    int cls;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    ProfScope(int c, cudaStream_t s) : cls(c), st(s) {
+        ++g_prof.launches[c];
+        if (g_prof.on) { a = g_prof.get(); cudaEventRecord(a, st); }
+    }
+    ~ProfScope() {
+        if (!a) return;
+        cudaEvent_t b = g_prof.get();
+        cudaEventRecord(b, st);
+        g_prof.pend.push_back({cls, a, b});
+        if (g_prof.pend.size() > 4096) g_prof.fold();
+    }
+};
+}  // namespace
+#define LAUNCH(cls, st, ...)            \
+    do {                                \
+        ProfScope ps_((cls), (st));     \
+        __VA_ARGS__;                    \
+    } while (0)
+
+extern "C" void pins_prof_enable(int32_t on) { g_prof.on = on != 0; }
+extern "C" void pins_prof_reset(void) {
+    g_prof.fold();
+    for (int c = 0; c < PINS_PROF_NCLASS; ++c) { g_prof.launches[c] = 0; g_prof.ms[c] = 0.0; }
+}
+extern "C" int pins_prof_read(int32_t cls, int64_t *launches, double *ms) {
+    PINS_ARG(cls >= 0 && cls < PINS_PROF_NCLASS && launches && ms, "class / pointers");
+    g_prof.fold();
+    *launches = g_prof.launches[cls];
+    *ms = g_prof.ms[cls];
+    return PINS_OK;
+}
 
 namespace {
 
@@ -164,19 +232,19 @@ template <bool SP, bool TR>
 cudaError_t launch_eval_t(int kind, int d, int G, cudaStream_t st, const EvalArgs &A) {
     dim3 grid(G), block(kThreads);
     const int dm = dmax_for(d);
-    if (kind == 0) eval_kernel<0, 0, SP, TR><<<grid, block, 0, st>>>(A);
+    if (kind == 0) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<0, 0, SP, TR><<<grid, block, 0, st>>>(A));
     else if (kind == 3) {
-        if constexpr (SP && !TR) eval_kernel<3, 0, true, false><<<grid, block, 0, st>>>(A);
+        if constexpr (SP && !TR) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<3, 0, true, false><<<grid, block, 0, st>>>(A));
     } else if (kind == 1) {
-        if (dm == 2) eval_kernel<1, 2, SP, TR><<<grid, block, 0, st>>>(A);
-        else if (dm == 3) eval_kernel<1, 3, SP, TR><<<grid, block, 0, st>>>(A);
-        else if (dm == 10) eval_kernel<1, 10, SP, TR><<<grid, block, 0, st>>>(A);
-        else eval_kernel<1, 16, SP, TR><<<grid, block, 0, st>>>(A);
+        if (dm == 2) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<1, 2, SP, TR><<<grid, block, 0, st>>>(A));
+        else if (dm == 3) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<1, 3, SP, TR><<<grid, block, 0, st>>>(A));
+        else if (dm == 10) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<1, 10, SP, TR><<<grid, block, 0, st>>>(A));
+        else LAUNCH(PINS_PROF_EVAL, st, eval_kernel<1, 16, SP, TR><<<grid, block, 0, st>>>(A));
     } else {
-        if (dm == 2) eval_kernel<2, 2, SP, TR><<<grid, block, 0, st>>>(A);
-        else if (dm == 3) eval_kernel<2, 3, SP, TR><<<grid, block, 0, st>>>(A);
-        else if (dm == 10) eval_kernel<2, 10, SP, TR><<<grid, block, 0, st>>>(A);
-        else eval_kernel<2, 16, SP, TR><<<grid, block, 0, st>>>(A);
+        if (dm == 2) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<2, 2, SP, TR><<<grid, block, 0, st>>>(A));
+        else if (dm == 3) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<2, 3, SP, TR><<<grid, block, 0, st>>>(A));
+        else if (dm == 10) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<2, 10, SP, TR><<<grid, block, 0, st>>>(A));
+        else LAUNCH(PINS_PROF_EVAL, st, eval_kernel<2, 16, SP, TR><<<grid, block, 0, st>>>(A));
     }
     return cudaGetLastError();
 }
@@ -198,8 +266,8 @@ cudaError_t launch_sweep(int kind, int d, long long m, long long n, cudaStream_t
     const int col_blocks = (int)std::min<long long>((n + 31) / 32, (long long)nsm * 8);
 #define SWEEP_PAIR(KD, DM)                                                  \
     do {                                                                    \
-        sweep_row_kernel<KD, DM><<<rows_blocks, kThreads, 0, st>>>(A);     \
-        sweep_col_kernel<KD, DM><<<col_blocks, kThreads, 0, st>>>(A);      \
+        LAUNCH(PINS_PROF_SWEEP_ROW, st, sweep_row_kernel<KD, DM><<<rows_blocks, kThreads, 0, st>>>(A));     \
+        LAUNCH(PINS_PROF_SWEEP_COL, st, sweep_col_kernel<KD, DM><<<col_blocks, kThreads, 0, st>>>(A));      \
     } while (0)
     if (kind == 0) SWEEP_PAIR(0, 0);
     else if (kind == 1) {
@@ -337,16 +405,16 @@ int run_eval(pins_workspace *ws, const pins_problem *pb, const double *phi, cons
         A.rb_col = ptr<int>(ws->rb_col);
         A.rb_val = ptr<double>(ws->rb_val);
         PINS_CUDA(launch_eval(sparse, trial, pb->cost_kind, pb->d, ws->G, st, A));
-        colsum_kernel<<<grid_1d(pb->n, ws->nsm), 256, 0, st>>>(
-            pb->n, ws->G, ptr<double>(ws->colpart), pb->b, ptr<double>(ws->colsum), ptr<double>(ws->gradg));
+        LAUNCH(PINS_PROF_REDUCE, st, colsum_kernel<<<grid_1d(pb->n, ws->nsm), 256, 0, st>>>(
+            pb->n, ws->G, ptr<double>(ws->colpart), pb->b, ptr<double>(ws->colsum), ptr<double>(ws->gradg)));
         PINS_CUDA(cudaGetLastError());
-        stats_kernel<<<1, 1024, 0, st>>>(pb->m, pb->n, ws->G, ptr<double>(ws->gradf),
+        LAUNCH(PINS_PROF_REDUCE, st, stats_kernel<<<1, 1024, 0, st>>>(pb->m, pb->n, ws->G, ptr<double>(ws->gradf),
                                          ptr<double>(ws->gradg), ptr<double>(ws->rowsum),
                                          ptr<double>(ws->blk), sparse ? ptr<int>(ws->rowcnt) : nullptr,
-                                         ws->cap, ptr<double>(ws->st));
+                                         ws->cap, ptr<double>(ws->st)));
         PINS_CUDA(cudaGetLastError());
-        dots_kernel<<<1, 1024, 0, st>>>(pb->m, pb->n, pb->a, f, pb->b, g, ptr<double>(ws->rowsum),
-                                        ptr<double>(ws->colsum), ptr<double>(ws->st));
+        LAUNCH(PINS_PROF_REDUCE, st, dots_kernel<<<1, 1024, 0, st>>>(pb->m, pb->n, pb->a, f, pb->b, g, ptr<double>(ws->rowsum),
+                                        ptr<double>(ws->colsum), ptr<double>(ws->st)));
         PINS_CUDA(cudaGetLastError());
         PINS_CUDA(cudaMemcpyAsync(ws->h, ws->st.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, st));
         PINS_CUDA(cudaStreamSynchronize(st));
@@ -370,11 +438,11 @@ int run_eval(pins_workspace *ws, const pins_problem *pb, const double *phi, cons
             const long long nnz = (long long)out->nnz;
             PINS_TRY(ensure(ws->colidx, sizeof(int) * std::max<long long>(nnz, 1)));
             PINS_TRY(ensure(ws->val, sizeof(double) * std::max<long long>(nnz, 1)));
-            scan_counts_kernel<<<1, 1024, 0, st>>>(pb->m, ptr<int>(ws->rowcnt), ws->cap,
-                                                   ptr<long long>(ws->rowptr));
-            csr_copy_kernel<<<grid_1d(pb->m * 32, ws->nsm), 256, 0, st>>>(
+            LAUNCH(PINS_PROF_CSR, st, scan_counts_kernel<<<1, 1024, 0, st>>>(pb->m, ptr<int>(ws->rowcnt), ws->cap,
+                                                   ptr<long long>(ws->rowptr)));
+            LAUNCH(PINS_PROF_CSR, st, csr_copy_kernel<<<grid_1d(pb->m * 32, ws->nsm), 256, 0, st>>>(
                 pb->m, ws->cap, ptr<long long>(ws->rowptr), ptr<int>(ws->rb_col),
-                ptr<double>(ws->rb_val), ptr<int>(ws->colidx), ptr<double>(ws->val));
+                ptr<double>(ws->rb_val), ptr<int>(ws->colidx), ptr<double>(ws->val)));
             PINS_CUDA(cudaGetLastError());
             ws->nnz = nnz;
             ws->csr_ready = true;
@@ -401,13 +469,13 @@ int build_csc(pins_workspace *ws, long long m, long long n, const long long *row
     PINS_CUDA(cudaMemsetAsync(ws->colcnt.p, 0, sizeof(int) * n, st));
     PINS_CUDA(cudaMemsetAsync(ws->cursor.p, 0, sizeof(int) * n, st));
     const int gw = grid_1d(m * 32, ws->nsm);
-    csc_count_kernel<<<gw, 256, 0, st>>>(m, rowptr, colidx, ptr<int>(ws->colcnt));
-    scan_counts_kernel<<<1, 1024, 0, st>>>(n, ptr<int>(ws->colcnt), 1LL << 40,
-                                           ptr<long long>(ws->colptr));
-    csc_fill_kernel<<<gw, 256, 0, st>>>(m, rowptr, colidx, val, ptr<long long>(ws->colptr),
-                                        ptr<int>(ws->cursor), ptr<int>(ws->rowidx), ptr<double>(ws->valT));
-    csc_sort_kernel<<<grid_1d(n, ws->nsm), 256, 0, st>>>(n, ptr<long long>(ws->colptr),
-                                                         ptr<int>(ws->rowidx), ptr<double>(ws->valT));
+    LAUNCH(PINS_PROF_CSR, st, csc_count_kernel<<<gw, 256, 0, st>>>(m, rowptr, colidx, ptr<int>(ws->colcnt)));
+    LAUNCH(PINS_PROF_CSR, st, scan_counts_kernel<<<1, 1024, 0, st>>>(n, ptr<int>(ws->colcnt), 1LL << 40,
+                                           ptr<long long>(ws->colptr)));
+    LAUNCH(PINS_PROF_CSR, st, csc_fill_kernel<<<gw, 256, 0, st>>>(m, rowptr, colidx, val, ptr<long long>(ws->colptr),
+                                        ptr<int>(ws->cursor), ptr<int>(ws->rowidx), ptr<double>(ws->valT)));
+    LAUNCH(PINS_PROF_CSR, st, csc_sort_kernel<<<grid_1d(n, ws->nsm), 256, 0, st>>>(n, ptr<long long>(ws->colptr),
+                                                         ptr<int>(ws->rowidx), ptr<double>(ws->valT)));
     PINS_CUDA(cudaGetLastError());
     return PINS_OK;
 }
@@ -458,7 +526,9 @@ int run_cg(pins_workspace *ws, long long m, long long n, const long long *rowptr
     A.b = b;
     A.st = ptr<double>(ws->cgst);
     void *args[] = {&A};
-    PINS_CUDA(cudaLaunchCooperativeKernel((void *)cg_kernel, dim3(G), dim3(kThreads), args, 0, st));
+    cudaError_t e_cg = cudaSuccess;
+    LAUNCH(PINS_PROF_CG, st, e_cg = cudaLaunchCooperativeKernel((void *)cg_kernel, dim3(G), dim3(kThreads), args, 0, st));
+    PINS_CUDA(e_cg);
     return PINS_OK;
 }
 
@@ -486,8 +556,8 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
     PINS_TRY(build_csc(ws, m, n, ptr<long long>(ws->rowptr), ptr<int>(ws->colidx),
                        ptr<double>(ws->val), ws->nnz, st));
     double *rhs = ptr<double>(ws->rhs);
-    scale_concat_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(m, n, pb->eta, ptr<double>(ws->gradf),
-                                                              ptr<double>(ws->gradg), rhs);
+    LAUNCH(PINS_PROF_VEC, st, scale_concat_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(m, n, pb->eta, ptr<double>(ws->gradf),
+                                                              ptr<double>(ws->gradg), rhs));
     PINS_CUDA(cudaGetLastError());
     const double mu = prm->mu_rel * std::max(cur->maxr, cur->maxc);
     const double rtol = cg_rtol(prm, cur->gnorm);
@@ -507,9 +577,9 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
     if (slope > 0.0 && std::isfinite(slope)) {
         for (int t = 0; t < prm->max_backtracks; ++t) {
             ++trials;
-            trial_prep_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(
+            LAUNCH(PINS_PROF_VEC, st, trial_prep_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(
                 m, n, alpha, 1.0 / pb->eta, f, g, d, ptr<double>(ws->ft), ptr<double>(ws->gt),
-                ptr<double>(ws->eu), ptr<double>(ws->ev));
+                ptr<double>(ws->eu), ptr<double>(ws->ev)));
             PINS_CUDA(cudaGetLastError());
             PINS_TRY(run_eval(ws, pb, phi, psi, s, ptr<double>(ws->ft), ptr<double>(ws->gt), tau, true,
                               st, &e));
@@ -586,8 +656,8 @@ extern "C" int pins_center_init(const pins_problem *pb, double *phi, double *psi
     PINS_TRY(check_problem(pb));
     PINS_ARG(phi && psi && s_host, "phi, psi, s");
     cudaStream_t st = (cudaStream_t)stream;
-    center_init_kernel<<<grid_1d(pb->m + pb->n, 148), 256, 0, st>>>(pb->m, pb->n, pb->eta, pb->a, pb->b,
-                                                                    phi, psi);
+    LAUNCH(PINS_PROF_VEC, st, center_init_kernel<<<grid_1d(pb->m + pb->n, 148), 256, 0, st>>>(pb->m, pb->n, pb->eta, pb->a, pb->b,
+                                                                    phi, psi));
     PINS_CUDA(cudaGetLastError());
     *s_host = 1.0;
     return PINS_OK;
@@ -598,8 +668,8 @@ extern "C" int pins_center_update(const pins_problem *pb, double *phi, double *p
     PINS_TRY(check_problem(pb));
     PINS_ARG(phi && psi && s_host && f && g, "phi, psi, s, f, g");
     cudaStream_t st = (cudaStream_t)stream;
-    center_update_kernel<<<grid_1d(pb->m + pb->n, 148), 256, 0, st>>>(pb->m, pb->n, pb->eta, f, g, phi,
-                                                                      psi);
+    LAUNCH(PINS_PROF_VEC, st, center_update_kernel<<<grid_1d(pb->m + pb->n, 148), 256, 0, st>>>(pb->m, pb->n, pb->eta, f, g, phi,
+                                                                      psi));
     PINS_CUDA(cudaGetLastError());
     *s_host += 1.0;
     return PINS_OK;
@@ -718,10 +788,10 @@ extern "C" int pins_residuals(pins_workspace *ws, const pins_problem *pb, const 
     PINS_TRY(prepare(ws, pb));
     double *uu = u ? u : ptr<double>(ws->uv);
     double *vv = v ? v : ptr<double>(ws->uv) + m;
-    lp_duals_kernel<<<grid_1d(m + n, ws->nsm), 256, 0, st>>>(m, n, pb->eta, 1.0 / s, f, g, phi, psi, uu, vv);
+    LAUNCH(PINS_PROF_VEC, st, lp_duals_kernel<<<grid_1d(m + n, ws->nsm), 256, 0, st>>>(m, n, pb->eta, 1.0 / s, f, g, phi, psi, uu, vv));
     PINS_CUDA(cudaGetLastError());
-    dots_kernel<<<1, 1024, 0, st>>>(m, n, pb->a, uu, pb->b, vv, ptr<double>(ws->rowsum),
-                                    ptr<double>(ws->colsum), ptr<double>(ws->st));
+    LAUNCH(PINS_PROF_REDUCE, st, dots_kernel<<<1, 1024, 0, st>>>(m, n, pb->a, uu, pb->b, vv, ptr<double>(ws->rowsum),
+                                    ptr<double>(ws->colsum), ptr<double>(ws->st)));
     PINS_CUDA(cudaMemcpyAsync(ws->h, ws->st.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, st));
     PINS_CUDA(cudaStreamSynchronize(st));
     res_host[0] = e.gnorm;
@@ -753,11 +823,11 @@ extern "C" int pins_plan(const pins_problem *pb, const double *phi, const double
     const double inv_eta = 1.0 / pb->eta, w = s * pb->cost_scale / pb->eta;
     const int G = grid_1d(pb->m * pb->n, 148, 16);
     if (pb->cost_kind == 0)
-        plan_kernel<0, 0><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx);
+        LAUNCH(PINS_PROF_PLAN, st, plan_kernel<0, 0><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx));
     else if (pb->cost_kind == 1)
-        plan_kernel<1, 16><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx);
+        LAUNCH(PINS_PROF_PLAN, st, plan_kernel<1, 16><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx));
     else
-        plan_kernel<2, 16><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx);
+        LAUNCH(PINS_PROF_PLAN, st, plan_kernel<2, 16><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx));
     PINS_CUDA(cudaGetLastError());
     return PINS_OK;
 }
@@ -786,7 +856,11 @@ extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_r
     bool converged = false;
     EvalOut cur;
     double s_last = s;
+    FILE *trace = nullptr;
+    if (const char *tp = getenv("PINS_TRACE")) trace = fopen(tp, "w");
+    auto tk0 = std::chrono::steady_clock::now();
     for (k = 0; k < prm->K; ++k) {
+        const int cg0 = cg_its;
         if (!prm->warm_start && k > 0) {
             PINS_CUDA(cudaMemsetAsync(f, 0, sizeof(double) * m, st));
             PINS_CUDA(cudaMemsetAsync(g, 0, sizeof(double) * n, st));
@@ -799,6 +873,8 @@ extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_r
             ++t;
         }
         sweeps += t;
+        const double g_sink = cur.gnorm;
+        const double nnz0 = (double)ws->nnz;
         int tn = 0;
         while (cur.gnorm > prm->newton_tol && tn < prm->T2) {
             double info[8];
@@ -808,6 +884,12 @@ extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_r
             if (info[2] == 0.0) break;
         }
         newton_its += tn;
+        if (trace) {
+            auto tk1 = std::chrono::steady_clock::now();
+            fprintf(trace, "%d %d %d %d %.0f %.3e %.3e %.17g %.3f\n", k, t, tn, cg_its - cg0, nnz0, g_sink,
+                    cur.gnorm, cur.cost, std::chrono::duration<double, std::milli>(tk1 - tk0).count());
+            tk0 = tk1;
+        }
         if (res->obj_trace_host) res->obj_trace_host[k] = cur.cost;
         objs.push_back(cur.cost);
         res->obj = cur.cost;
@@ -823,6 +905,7 @@ extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_r
             break;
         }
     }
+    if (trace) fclose(trace);
     if (k > prm->K) k = prm->K;
     // LP dual estimates of X^{K} (reading R8): u = phi/s_last, v = psi/s_last
     // (phi, psi are already the updated centre; f, g folded in).
@@ -833,11 +916,11 @@ extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_r
         PINS_TRY(prepare(ws, pb));
         if (!uu) uu = ptr<double>(ws->uv);
         if (!vv) vv = ptr<double>(ws->uv) + m;
-        scale_concat_kernel<<<grid_1d(m + n, ws->nsm), 256, 0, st>>>(m, n, inv, phi, psi, ptr<double>(ws->dir));
+        LAUNCH(PINS_PROF_VEC, st, scale_concat_kernel<<<grid_1d(m + n, ws->nsm), 256, 0, st>>>(m, n, inv, phi, psi, ptr<double>(ws->dir)));
         PINS_CUDA(cudaMemcpyAsync(uu, ptr<double>(ws->dir), sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
         PINS_CUDA(cudaMemcpyAsync(vv, ptr<double>(ws->dir) + m, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-        dots_kernel<<<1, 1024, 0, st>>>(m, n, pb->a, uu, pb->b, vv, ptr<double>(ws->rowsum),
-                                        ptr<double>(ws->colsum), ptr<double>(ws->st));
+        LAUNCH(PINS_PROF_REDUCE, st, dots_kernel<<<1, 1024, 0, st>>>(m, n, pb->a, uu, pb->b, vv, ptr<double>(ws->rowsum),
+                                        ptr<double>(ws->colsum), ptr<double>(ws->st)));
         PINS_CUDA(cudaMemcpyAsync(ws->h, ws->st.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, st));
         PINS_CUDA(cudaStreamSynchronize(st));
         res->lp_dual_obj = ws->h[8];
@@ -850,5 +933,63 @@ extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_r
     res->cg_iters = cg_its;
     res->status = converged ? 0 : 1;
     res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return PINS_OK;
+}
+
+extern "C" int pins_solve_host(const pins_problem *pb_host, const pins_params *prm, pins_result *res_host,
+                               int64_t *io_bytes_host, void *stream) {
+    PINS_TRY(check_problem(pb_host));
+    PINS_ARG(prm && res_host && io_bytes_host, "params / result / io_bytes");
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long m = pb_host->m, n = pb_host->n;
+    pins_problem pb = *pb_host;
+    // one stream-ordered allocation for inputs and outputs
+    const bool dense = pb_host->cost_kind == PINS_COST_DENSE;
+    const long long nC = dense ? m * pb_host->ldc : 0;
+    const long long nx = dense ? 0 : m * (long long)pb_host->d, ny = dense ? 0 : n * (long long)pb_host->d;
+    const long long in_elems = nC + nx + ny + m + n;
+    const long long out_elems = 3 * (m + n);     // f g phi psi u v
+    double *buf = nullptr;
+    PINS_CUDA(cudaMallocAsync((void **)&buf, sizeof(double) * (in_elems + out_elems), st));
+    double *p = buf;
+    long long h2d = 0, d2h = 0;
+    auto up = [&](const double *src, long long cnt) -> double * {
+        double *dst = p;
+        p += cnt;
+        if (cnt) cudaMemcpyAsync(dst, src, sizeof(double) * cnt, cudaMemcpyHostToDevice, st);
+        h2d += sizeof(double) * cnt;
+        return dst;
+    };
+    if (dense) pb.C = up(pb_host->C, nC);
+    else {
+        pb.x = up(pb_host->x, nx);
+        pb.y = up(pb_host->y, ny);
+    }
+    pb.a = up(pb_host->a, m);
+    pb.b = up(pb_host->b, n);
+    PINS_CUDA(cudaGetLastError());
+    pins_result r = *res_host;
+    r.f = p; r.g = p + m; r.phi = p + m + n; r.psi = p + 2 * m + n; r.u = p + 2 * (m + n); r.v = p + 3 * m + 2 * n;
+    int rc = pins_solve(&pb, prm, &r, stream);
+    if (rc == PINS_OK) {
+        double *const srcs[6] = {r.f, r.g, r.phi, r.psi, r.u, r.v};
+        double *const dsts[6] = {res_host->f, res_host->g, res_host->phi, res_host->psi, res_host->u, res_host->v};
+        const long long cnts[6] = {m, n, m, n, m, n};
+        for (int q = 0; q < 6; ++q) {
+            if (!dsts[q]) continue;
+            cudaMemcpyAsync(dsts[q], srcs[q], sizeof(double) * cnts[q], cudaMemcpyDeviceToHost, st);
+            d2h += sizeof(double) * cnts[q];
+        }
+        double *const keep[6] = {res_host->f, res_host->g, res_host->phi, res_host->psi, res_host->u, res_host->v};
+        *res_host = r;
+        res_host->f = keep[0]; res_host->g = keep[1]; res_host->phi = keep[2];
+        res_host->psi = keep[3]; res_host->u = keep[4]; res_host->v = keep[5];
+    }
+    cudaFreeAsync(buf, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (rc != PINS_OK) return rc;
+    PINS_CUDA(e);
+    io_bytes_host[0] = h2d;
+    io_bytes_host[1] = d2h;
     return PINS_OK;
 }

@@ -22,6 +22,7 @@ EXPORTS = [
     "pins_default_params", "pins_workspace_create", "pins_workspace_destroy", "pins_last_error",
     "pins_center_init", "pins_center_update", "pins_sinkhorn_sweep", "pins_evaluate",
     "pins_get_csr", "pins_sparsify_dense", "pins_cg", "pins_newton_step", "pins_residuals", "pins_plan", "pins_solve",
+    "pins_prof_enable", "pins_prof_reset", "pins_prof_read", "pins_solve_host",
 ]
 
 
@@ -78,6 +79,10 @@ def load():
         "pins_residuals": (I32, [V, P, V, V, D, V, V, V, V, POINTER(D), V]),
         "pins_plan": (I32, [P, V, V, D, V, V, V, I64, V]),
         "pins_solve": (I32, [P, POINTER(Params), POINTER(Result), V]),
+        "pins_solve_host": (I32, [P, POINTER(Params), POINTER(Result), POINTER(I64), V]),
+        "pins_prof_enable": (None, [I32]),
+        "pins_prof_reset": (None, []),
+        "pins_prof_read": (I32, [I32, POINTER(I64), POINTER(D)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -268,4 +273,56 @@ def solve(pb: DeviceProblem, prm: Optional[Params] = None, trace: bool = False, 
     out.update(f=f, g=g, phi=phi, psi=psi, u=u, v=v)
     if trace:
         out["trace"] = [tr[i] for i in range(res.outer_iters)]
+    return out
+
+
+PROF_CLASSES = ["sweep_row", "sweep_col", "eval", "reduce", "csr", "cg", "vec", "plan"]
+
+
+def prof_enable(on: bool = True):
+    load().pins_prof_enable(1 if on else 0)
+
+
+def prof_reset():
+    load().pins_prof_reset()
+
+
+def prof_read() -> Dict[str, Dict]:
+    """{class: {"launches": L, "ms": device ms}} since the last prof_reset (synchronises)."""
+    lib = load()
+    out = {}
+    for c, name in enumerate(PROF_CLASSES):
+        n, ms = c_int64(), c_double()
+        _check(lib.pins_prof_read(c, ctypes.byref(n), ctypes.byref(ms)))
+        out[name] = {"launches": n.value, "ms": ms.value}
+    return out
+
+
+class HostProblem:
+    """Host (pinned) copy of an OT instance for the end-to-end path ``solve_host``."""
+
+    def __init__(self, w, eta=None):
+        torch = _torch()
+        pin = lambda v: None if v is None else torch.as_tensor(v, dtype=torch.float64).contiguous().pin_memory()
+        self.m, self.n = int(w.m), int(w.n)
+        self.a, self.b, self.C, self.x, self.y = pin(w.a), pin(w.b), pin(w.C), pin(w.X), pin(w.Y)
+        self.struct = Problem(
+            m=self.m, n=self.n, cost_kind=int(w.kind), d=0 if w.X is None else int(w.X.shape[1]),
+            C=_p(self.C), ldc=0 if self.C is None else int(self.C.stride(0)), x=_p(self.x), y=_p(self.y),
+            cost_scale=float(w.cost_scale), a=_p(self.a), b=_p(self.b), eta=float(w.eta if eta is None else eta))
+        self.u = torch.empty(self.m, dtype=torch.float64).pin_memory()
+        self.v = torch.empty(self.n, dtype=torch.float64).pin_memory()
+
+
+def solve_host(hp: HostProblem, prm: Optional[Params] = None) -> Dict:
+    """End-to-end pins_solve_host: inputs copied from pinned host memory, LP duals u, v
+    copied back into hp.u / hp.v; returns the scalars plus h2d / d2h byte counts."""
+    prm = prm or default_params()
+    res = Result(u=_p(hp.u), v=_p(hp.v))
+    io = (c_int64 * 2)()
+    _check(load().pins_solve_host(ctypes.byref(hp.struct), ctypes.byref(prm), ctypes.byref(res), io, _stream()))
+    out = {k: getattr(res, k) for k in ("s", "obj", "dual_obj", "lp_dual_obj", "kkt", "dual_inf", "gap",
+                                        "outer_iters", "sweeps", "newton_iters", "cg_iters", "status",
+                                        "seconds")}
+    out.update(h2d_bytes=io[0], d2h_bytes=io[1])
     return out
