@@ -12,6 +12,9 @@
 
 #include "pins.h"
 #include "pins_kernels.cuh"
+#include "pins_pass.cuh"
+#include "pins_cg.cuh"
+#include "pins_order.cuh"
 
 using namespace pins;
 
@@ -134,10 +137,23 @@ T *ptr(DevBuf &b) { return reinterpret_cast<T *>(b.p); }
 
 }  // namespace
 
+struct SideBufs {
+    DevBuf pa, pb, pj, psc, blk, blkoff, ticket, cnt, bcol, bval, jstar;
+};
+
 struct pins_workspace {
     DevBuf colpart, blk, rowsum, gradf, colsum, gradg, rowcnt, rb_col, rb_val;
     DevBuf rowptr, colidx, val, colcnt, colptr, cursor, rowidx, valT;
-    DevBuf cgvec, cgpart, cgst, st, ft, gt, eu, ev, dir, rhs, tab, fsave, gsave, uv;
+    DevBuf cgvec, cgpart, cgst, st, ft, gt, eu, ev, bu, bv, dir, rhs, tab, fsave, gsave, uv;
+    // v2 dense passes
+    SideBufs sb[2];
+    DevBuf x32, y32, x64, y64, nx32, ny32, pinfo, ctl, gticket, pst, tol;
+    const void *key_C = nullptr, *key_x = nullptr, *key_y = nullptr;
+    long long key_m = -1, key_n = -1, key_ldc = -1;
+    int key_kind = -1, key_d = -1;
+    int cost_row = 0, cost_col = 0, dp = 4;
+    int S[2] = {1, 1};
+    long long pcap = 16;       // per (row, split) sparsify capacity
     long long m = 0, n = 0, cap = 64, nnz = 0;
     int G = 0, nsm = 0, dev = -1;
     bool csr_ready = false, csc_ready = false;
@@ -188,9 +204,17 @@ extern "C" void pins_workspace_destroy(pins_workspace *ws) {
                       &ws->rowcnt, &ws->rb_col, &ws->rb_val, &ws->rowptr, &ws->colidx, &ws->val,
                       &ws->colcnt, &ws->colptr, &ws->cursor, &ws->rowidx, &ws->valT, &ws->cgvec,
                       &ws->cgpart, &ws->cgst, &ws->st, &ws->ft, &ws->gt, &ws->eu, &ws->ev,
-                      &ws->dir, &ws->rhs, &ws->tab, &ws->fsave, &ws->gsave, &ws->uv};
+                      &ws->dir, &ws->rhs, &ws->tab, &ws->fsave, &ws->gsave, &ws->uv, &ws->bu, &ws->bv,
+                      &ws->x32, &ws->y32, &ws->x64, &ws->y64, &ws->nx32, &ws->ny32, &ws->pinfo,
+                      &ws->ctl, &ws->gticket, &ws->pst, &ws->tol};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
+    for (int q = 0; q < 2; ++q) {
+        SideBufs &B = ws->sb[q];
+        DevBuf *sbufs[] = {&B.pa, &B.pb, &B.pj, &B.psc, &B.blk, &B.blkoff, &B.ticket, &B.cnt, &B.bcol, &B.bval, &B.jstar};
+        for (DevBuf *b : sbufs)
+            if (b->p) cudaFree(b->p);
+    }
     if (ws->h) cudaFreeHost(ws->h);
     delete ws;
 }
@@ -373,9 +397,9 @@ struct EvalOut {
     double gnorm, sumX, cost, dualP, nnz, maxz, maxcnt, em1, maxr, maxc, af;
 };
 
-// One evaluation pass (+ optional sparsify, + optional trial term).  Grows the
-// row-buffer capacity and re-runs on overflow.  Synchronises the stream.
-int run_eval(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi,
+// Legacy evaluation pass (one CTA per row range, ballot compaction); used
+// only by pins_sparsify_dense, whose "cost" is the caller's plan (KIND 3).
+int run_eval_legacy(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi,
              double s, const double *f, const double *g, double tau, bool trial,
              cudaStream_t st, EvalOut *out) {
     PINS_TRY(prepare(ws, pb));
@@ -459,6 +483,331 @@ int run_eval(pins_workspace *ws, const pins_problem *pb, const double *phi, cons
     return PINS_ERR_NUMERIC;
 }
 
+
+// ===================================================================== v2
+// Thread-per-row dense passes (pins_pass.cuh).
+int dp_for(int d) { return d <= 4 ? 4 : d <= 12 ? 12 : 16; }
+
+// (Re)build the derived cost data when the problem identity changes: padded
+// fp32 / fp64 point copies, norms, the exact-fp32 decision, argmax seeds.
+int prepare_pass(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
+    const long long m = pb->m, n = pb->n;
+    const bool same = ws->key_C == pb->C && ws->key_x == pb->x && ws->key_y == pb->y && ws->key_m == m &&
+                      ws->key_n == n && ws->key_kind == pb->cost_kind && ws->key_d == pb->d &&
+                      ws->key_ldc == pb->ldc;
+    for (int q = 0; q < 2; ++q) {
+        const long long M = q == 0 ? m : n, N = q == 0 ? n : m;
+        const int RB = (int)((M + kPT - 1) / kPT);
+        // column splits: ~4 CTAs of 128 threads per SM per side, splits >= kCC columns
+        long long S = (4LL * ws->nsm + RB - 1) / RB;
+        S = std::max(1LL, std::min(S, std::max(1LL, N / kCC)));
+        ws->S[q] = (int)S;
+        SideBufs &B = ws->sb[q];
+        PINS_TRY(ensure(B.pa, sizeof(double) * S * M));
+        PINS_TRY(ensure(B.pb, sizeof(double) * S * M));
+        PINS_TRY(ensure(B.pj, sizeof(int) * S * M));
+        PINS_TRY(ensure(B.psc, sizeof(double) * S * RB * 4));
+        PINS_TRY(ensure(B.blk, sizeof(double) * RB * 8));
+        PINS_TRY(ensure(B.blkoff, sizeof(long long) * (RB + 1)));
+        PINS_TRY(ensure(B.cnt, sizeof(int) * S * M));
+        if (B.ticket.bytes < sizeof(unsigned) * RB) {
+            PINS_TRY(ensure(B.ticket, sizeof(unsigned) * RB));
+            PINS_CUDA(cudaMemsetAsync(B.ticket.p, 0, B.ticket.bytes, st));
+        }
+        if (B.jstar.bytes < sizeof(int) * M || !same) {
+            PINS_TRY(ensure(B.jstar, sizeof(int) * M));
+            PINS_CUDA(cudaMemsetAsync(B.jstar.p, 0xff, sizeof(int) * M, st));
+        }
+    }
+    if (ws->gticket.bytes == 0) {
+        PINS_TRY(ensure(ws->gticket, 64));
+        PINS_CUDA(cudaMemsetAsync(ws->gticket.p, 0, 64, st));
+    }
+    PINS_TRY(ensure(ws->pst, sizeof(double) * 32));
+    PINS_TRY(ensure(ws->ctl, sizeof(int) * 8));
+    PINS_TRY(ensure(ws->tol, sizeof(double) * 4));
+    PINS_TRY(ensure(ws->bu, sizeof(double) * m));
+    PINS_TRY(ensure(ws->bv, sizeof(double) * n));
+    if (same) return PINS_OK;
+    if (pb->cost_kind == PINS_COST_DENSE) {
+        ws->cost_row = PC_DENSE_ROW;
+        ws->cost_col = PC_DENSE_COL;
+        ws->dp = 4;
+    } else {
+        const int dp = dp_for(pb->d);
+        ws->dp = dp;
+        PINS_TRY(ensure(ws->x32, sizeof(float) * m * dp));
+        PINS_TRY(ensure(ws->y32, sizeof(float) * n * dp));
+        PINS_TRY(ensure(ws->x64, sizeof(double) * m * dp));
+        PINS_TRY(ensure(ws->y64, sizeof(double) * n * dp));
+        PINS_TRY(ensure(ws->nx32, sizeof(float) * m));
+        PINS_TRY(ensure(ws->ny32, sizeof(float) * n));
+        PINS_TRY(ensure(ws->pinfo, sizeof(unsigned long long) * 8));
+        PINS_CUDA(cudaMemsetAsync(ws->pinfo.p, 0, sizeof(unsigned long long) * 8, st));
+        unsigned long long *info = ptr<unsigned long long>(ws->pinfo);
+        LAUNCH(PINS_PROF_VEC, st, prep_points_kernel<<<grid_1d(m, ws->nsm), 256, 0, st>>>(
+            m, pb->d, dp, pb->x, ptr<float>(ws->x32), ptr<double>(ws->x64), ptr<float>(ws->nx32), info));
+        LAUNCH(PINS_PROF_VEC, st, prep_points_kernel<<<grid_1d(n, ws->nsm), 256, 0, st>>>(
+            n, pb->d, dp, pb->y, ptr<float>(ws->y32), ptr<double>(ws->y64), ptr<float>(ws->ny32), info + 4));
+        PINS_CUDA(cudaGetLastError());
+        unsigned long long hi[8];
+        PINS_CUDA(cudaMemcpyAsync(hi, info, sizeof hi, cudaMemcpyDeviceToHost, st));
+        PINS_CUDA(cudaStreamSynchronize(st));
+        double ax, nxm, ay, nym;
+        memcpy(&ax, &hi[0], 8); memcpy(&nxm, &hi[1], 8); memcpy(&ay, &hi[4], 8); memcpy(&nym, &hi[5], 8);
+        const bool integral = hi[2] == 0 && hi[6] == 0;
+        const double two24 = 16777216.0;
+        bool exact32;
+        if (pb->cost_kind == PINS_COST_SQEUCLID) {
+            const double bound = (std::sqrt(nxm) + std::sqrt(nym)) * (std::sqrt(nxm) + std::sqrt(nym));
+            exact32 = integral && bound < two24 && ax < two24 && ay < two24;
+            ws->cost_row = ws->cost_col = exact32 ? PC_SQ32 : PC_SQ64;
+        } else {
+            exact32 = integral && 2.0 * pb->d * std::max(ax, ay) < two24;
+            ws->cost_row = ws->cost_col = exact32 ? PC_L132 : PC_L164;
+        }
+    }
+    ws->key_C = pb->C; ws->key_x = pb->x; ws->key_y = pb->y; ws->key_m = m; ws->key_n = n;
+    ws->key_kind = pb->cost_kind; ws->key_d = pb->d; ws->key_ldc = pb->ldc;
+    return PINS_OK;
+}
+
+// Fill the pass description of one orientation (0: rows of X, 1: columns).
+void fill_side(pins_workspace *ws, const pins_problem *pb, int o, const double *f, const double *phi,
+               const double *g, const double *psi, PassSide &P) {
+    memset(&P, 0, sizeof P);
+    const bool row = o == 0;
+    P.M = row ? pb->m : pb->n;
+    P.N = row ? pb->n : pb->m;
+    P.S = ws->S[o];
+    P.RB = (int)((P.M + kPT - 1) / kPT);
+    P.dp = ws->dp;
+    P.C = pb->C;
+    P.ldc = pb->ldc;
+    P.xr32 = ptr<float>(row ? ws->x32 : ws->y32);
+    P.yc32 = ptr<float>(row ? ws->y32 : ws->x32);
+    P.nxr = ptr<float>(row ? ws->nx32 : ws->ny32);
+    P.nyc = ptr<float>(row ? ws->ny32 : ws->nx32);
+    P.xr64 = ptr<double>(row ? ws->x64 : ws->y64);
+    P.yc64 = ptr<double>(row ? ws->y64 : ws->x64);
+    P.fr = row ? f : g;
+    P.phir = row ? phi : psi;
+    P.gc = row ? g : f;
+    P.psic = row ? psi : phi;
+    P.m1_row = row ? 1 : 0;
+    P.ar = row ? pb->a : pb->b;
+    SideBufs &B = ws->sb[o];
+    P.jstar = ptr<int>(B.jstar);
+    P.pa = ptr<double>(B.pa);
+    P.pb = ptr<double>(B.pb);
+    P.pj = ptr<int>(B.pj);
+    P.psc = ptr<double>(B.psc);
+    P.blk = ptr<double>(B.blk);
+    P.blkoff = ptr<long long>(B.blkoff);
+    P.ticket = ptr<unsigned>(B.ticket);
+    P.cnt = ptr<int>(B.cnt);
+    P.bcol = ptr<int>(B.bcol);
+    P.bval = ptr<double>(B.bval);
+    P.cap = ws->pcap;
+    P.sum = ptr<double>(row ? ws->rowsum : ws->colsum);
+    P.grad = ptr<double>(row ? ws->gradf : ws->gradg);
+}
+
+#define PINS_DP_DISPATCH(DPV, ...)          \
+    do {                                    \
+        if ((DPV) == 4) {                   \
+            constexpr int DP = 4;           \
+            __VA_ARGS__;                    \
+        } else if ((DPV) == 12) {           \
+            constexpr int DP = 12;          \
+            __VA_ARGS__;                    \
+        } else {                            \
+            constexpr int DP = 16;          \
+            __VA_ARGS__;                    \
+        }                                   \
+    } while (0)
+
+cudaError_t launch_lse(int cost, int dp, int grid, cudaStream_t st, const PassArgs &A) {
+    switch (cost) {
+        case PC_DENSE_ROW: LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_DENSE_ROW, 4><<<grid, kPT, 0, st>>>(A)); break;
+        case PC_DENSE_COL: LAUNCH(PINS_PROF_SWEEP_COL, st, lse_pass_kernel<PC_DENSE_COL, 4><<<grid, kPT, 0, st>>>(A)); break;
+        case PC_SQ32: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_SQ32, DP><<<grid, kPT, 0, st>>>(A))); break;
+        case PC_L132: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_L132, DP><<<grid, kPT, 0, st>>>(A))); break;
+        case PC_SQ64: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_SQ64, DP><<<grid, kPT, 0, st>>>(A))); break;
+        default: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_L164, DP><<<grid, kPT, 0, st>>>(A))); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sum(int cost, int dp, int grid, cudaStream_t st, const PassArgs &A) {
+    switch (cost) {
+        case PC_DENSE_ROW: LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_DENSE_ROW, PC_DENSE_COL, 4><<<grid, kPT, 0, st>>>(A)); break;
+        case PC_SQ32: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_SQ32, PC_SQ32, DP><<<grid, kPT, 0, st>>>(A))); break;
+        case PC_L132: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_L132, PC_L132, DP><<<grid, kPT, 0, st>>>(A))); break;
+        case PC_SQ64: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_SQ64, PC_SQ64, DP><<<grid, kPT, 0, st>>>(A))); break;
+        default: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_L164, PC_L164, DP><<<grid, kPT, 0, st>>>(A))); break;
+    }
+    return cudaGetLastError();
+}
+
+void base_args(pins_workspace *ws, const pins_problem *pb, double s, PassArgs &A) {
+    memset(&A, 0, sizeof A);
+    A.eta = pb->eta;
+    A.inv_eta = 1.0 / pb->eta;
+    A.w = s * pb->cost_scale / pb->eta;
+    A.tab = ptr<ExpTable>(ws->tab);
+    A.gticket = ptr<unsigned>(ws->gticket);
+    A.st = ptr<double>(ws->pst);
+    A.ctl = ptr<int>(ws->ctl);
+}
+
+// One Sinkhorn half-sweep: o = 0 updates f (Alg. 2 line 5), o = 1 updates g (line 6).
+int half_sweep(pins_workspace *ws, const pins_problem *pb, int o, const double *phi, const double *psi,
+               double s, double *f, double *g, bool check_done, bool test_tol, cudaStream_t st) {
+    PassArgs A;
+    base_args(ws, pb, s, A);
+    fill_side(ws, pb, o, f, phi, g, psi, A.side[0]);
+    A.side[0].fout = o == 0 ? f : g;
+    A.side[0].fsave = o == 0 ? ptr<double>(ws->fsave) : nullptr;
+    A.nsides = 1;
+    A.G0 = A.side[0].S * A.side[0].RB;
+    A.check_done = check_done ? 1 : 0;
+    A.count_sweep = o == 1 ? 1 : 0;
+    A.test_tol = test_tol ? 1 : 0;
+    A.sink_tol = ptr<double>(ws->tol);
+    const int cost = o == 0 ? ws->cost_row : ws->cost_col;
+    PINS_CUDA(launch_lse(cost, ws->dp, A.G0, st, A));
+    return PINS_OK;
+}
+
+int do_sweep(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi,
+             double s, double *f, double *g, cudaStream_t st) {
+    PINS_TRY(prepare_pass(ws, pb, st));
+    PINS_TRY(ensure(ws->fsave, sizeof(double) * std::max(pb->m, pb->n)));
+    PINS_TRY(half_sweep(ws, pb, 0, phi, psi, s, f, g, false, false, st));
+    PINS_TRY(half_sweep(ws, pb, 1, phi, psi, s, f, g, false, false, st));
+    return PINS_OK;
+}
+
+// Sinkhorn phase of Alg. 2 (lines 4-8) on the device: sweeps are queued in
+// batches without host round trips; every row half-sweep after the first
+// also computes the residual of the iterate it starts from and, when that is
+// <= sink_tol, flags the phase done and rolls its own update back (so the
+// phase stops at exactly the first iterate with residual <= sink_tol, as the
+// oracle does); queued kernels see the flag and exit.  res0 is the full
+// residual of the starting point (the caller's evaluation).  Returns sweeps.
+int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params *prm, const double *phi,
+                   const double *psi, double s, double *f, double *g, double res0, int *sweeps_out,
+                   cudaStream_t st) {
+    *sweeps_out = 0;
+    if (res0 <= prm->sink_tol || prm->T1 <= 0) return PINS_OK;
+    PINS_TRY(prepare_pass(ws, pb, st));
+    PINS_TRY(ensure(ws->fsave, sizeof(double) * std::max(pb->m, pb->n)));
+    double tolv = prm->sink_tol;
+    PINS_CUDA(cudaMemcpyAsync(ws->tol.p, &tolv, sizeof(double), cudaMemcpyHostToDevice, st));
+    PINS_CUDA(cudaMemsetAsync(ws->ctl.p, 0, sizeof(int) * 8, st));
+    int done = 0, batch = 1, queued = 0;
+    while (!done && queued < prm->T1) {
+        const int nb = std::min(batch, prm->T1 - queued);
+        for (int q = 0; q < nb; ++q) {
+            const bool first = (queued + q) == 0;
+            PINS_TRY(half_sweep(ws, pb, 0, phi, psi, s, f, g, true, !first, st));
+            PINS_TRY(half_sweep(ws, pb, 1, phi, psi, s, f, g, true, false, st));
+        }
+        queued += nb;
+        int *hc = reinterpret_cast<int *>(ws->h + 40);
+        PINS_CUDA(cudaMemcpyAsync(hc, ws->ctl.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+        PINS_CUDA(cudaStreamSynchronize(st));
+        done = hc[0];
+        *sweeps_out = hc[1];
+        if (done && hc[2]) {   // roll back the f update of the half-sweep that found convergence
+            PINS_CUDA(cudaMemcpyAsync(f, ws->fsave.p, sizeof(double) * pb->m, cudaMemcpyDeviceToDevice, st));
+        }
+        batch = std::min(batch * 2, 64);
+    }
+    return PINS_OK;
+}
+
+// Evaluation of X~(f, g) (Eq. (7)) in both orientations: sums, gradient,
+// objectives; with tau > 0 also the sparsified CSR (rows) and CSC (columns).
+// Grows the per-(row, split) capacity and re-runs on overflow.  Synchronises.
+int run_eval(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi, double s,
+             const double *f, const double *g, double tau, bool trial, cudaStream_t st, EvalOut *out) {
+    PINS_TRY(prepare(ws, pb));
+    PINS_TRY(prepare_pass(ws, pb, st));
+    const bool sparse = tau > 0.0;
+    for (int attempt = 0; attempt < 6; ++attempt) {
+        for (int q = 0; q < 2; ++q) {
+            const long long M = q == 0 ? pb->m : pb->n;
+            if (sparse) {
+                PINS_TRY(ensure(ws->sb[q].bcol, sizeof(int) * M * ws->S[q] * ws->pcap));
+                PINS_TRY(ensure(ws->sb[q].bval, sizeof(double) * M * ws->S[q] * ws->pcap));
+            }
+        }
+        PassArgs A;
+        base_args(ws, pb, s, A);
+        fill_side(ws, pb, 0, f, phi, g, psi, A.side[0]);
+        fill_side(ws, pb, 1, f, phi, g, psi, A.side[1]);
+        A.nsides = 2;
+        A.G0 = A.side[0].S * A.side[0].RB;
+        const int G1 = A.side[1].S * A.side[1].RB;
+        A.side[0].want_cx = 1;
+        A.side[0].tau = A.side[1].tau = tau;
+        if (trial) {
+            A.side[0].eu = ptr<double>(ws->eu);
+            A.side[0].ev = ptr<double>(ws->ev);
+            A.side[0].bu = ptr<double>(ws->bu);
+            A.side[0].bv = ptr<double>(ws->bv);
+        }
+        A.a_dot = pb->a; A.f_dot = f; A.b_dot = pb->b; A.g_dot = g;
+        PINS_CUDA(launch_sum(ws->cost_row, ws->dp, A.G0 + G1, st, A));
+        PINS_CUDA(cudaMemcpyAsync(ws->h, ws->pst.p, 12 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        PINS_CUDA(cudaStreamSynchronize(st));
+        const double *h = ws->h;
+        out->gnorm = h[0] + h[1];
+        out->sumX = h[2];
+        out->cost = h[3] * pb->cost_scale;
+        out->em1 = h[4];
+        out->maxz = h[5];
+        out->maxcnt = h[6];
+        out->nnz = h[7];
+        out->af = h[8];
+        out->maxr = h[9];
+        out->maxc = h[10];
+        out->dualP = h[8] - pb->eta * h[2];
+        ws->csr_ready = ws->csc_ready = false;
+        if (!sparse) return PINS_OK;
+        if (out->maxcnt <= (double)ws->pcap) {
+            const long long nnz = (long long)h[7];
+            if ((long long)h[11] != nnz) {
+                snprintf(g_err, sizeof g_err, "CSR/CSC pattern mismatch (%lld vs %lld)", nnz, (long long)h[11]);
+                return PINS_ERR_NUMERIC;
+            }
+            PINS_TRY(ensure(ws->rowptr, sizeof(long long) * (pb->m + 1)));
+            PINS_TRY(ensure(ws->colptr, sizeof(long long) * (pb->n + 1)));
+            PINS_TRY(ensure(ws->colidx, sizeof(int) * std::max<long long>(nnz, 1)));
+            PINS_TRY(ensure(ws->val, sizeof(double) * std::max<long long>(nnz, 1)));
+            PINS_TRY(ensure(ws->rowidx, sizeof(int) * std::max<long long>(nnz, 1)));
+            PINS_TRY(ensure(ws->valT, sizeof(double) * std::max<long long>(nnz, 1)));
+            CsrOut O0{ptr<long long>(ws->rowptr), ptr<int>(ws->colidx), ptr<double>(ws->val),
+                      ptr<long long>(ws->sb[0].blkoff)};
+            CsrOut O1{ptr<long long>(ws->colptr), ptr<int>(ws->rowidx), ptr<double>(ws->valT),
+                      ptr<long long>(ws->sb[1].blkoff)};
+            LAUNCH(PINS_PROF_CSR, st, csr_build_kernel<<<A.side[0].RB + A.side[1].RB, kPT, 0, st>>>(
+                A.side[0], A.side[1], 2, O0, O1));
+            PINS_CUDA(cudaGetLastError());
+            ws->nnz = nnz;
+            ws->csr_ready = ws->csc_ready = true;
+            return PINS_OK;
+        }
+        long long c = ws->pcap;
+        while ((double)c < out->maxcnt) c *= 2;
+        ws->pcap = c;
+    }
+    snprintf(g_err, sizeof g_err, "sparsify capacity did not converge");
+    return PINS_ERR_NUMERIC;
+}
+
 int build_csc(pins_workspace *ws, long long m, long long n, const long long *rowptr,
               const int *colidx, const double *val, long long nnz, cudaStream_t st) {
     PINS_TRY(ensure(ws->colcnt, sizeof(int) * n));
@@ -532,6 +881,72 @@ int run_cg(pins_workspace *ws, long long m, long long n, const long long *rowptr
     return PINS_OK;
 }
 
+
+// ---- cluster-resident Schur-complement CG (pins_cg.cuh) ----
+constexpr long long kClusterNnzMax = 400000;       // above: the grid-wide kernel streams faster
+constexpr int kClusterSmem = 220 * 1024;           // dynamic shared memory per CTA
+// fixed part of the cluster kernel's shared memory (vectors, pointers, heavy lists)
+size_t cluster_cg_smem(long long m, long long n) {
+    const long long keep = std::min(m, n), elim = std::max(m, n);
+    const long long R = (keep + kCGC - 1) / kCGC, Cc = (elim + kCGC - 1) / kCGC;
+    return sizeof(double) * (size_t)(8 * R + 2 * Cc) + sizeof(int) * (size_t)(2 * R + 2 * Cc + 2) + 16;
+}
+bool use_cluster_cg(pins_workspace *ws, long long m, long long n) {
+    return ws->nnz <= kClusterNnzMax && cluster_cg_smem(m, n) <= (size_t)kClusterSmem - 16 * 1024 &&
+           ws->csc_ready;
+}
+
+// kept side = the smaller of (rows, columns); the other is eliminated exactly
+int run_cg_cluster(pins_workspace *ws, long long m, long long n, double mu, const double *rhs, double *x,
+                   double rtol, int maxit, const double *gradf, const double *gradg, const double *a,
+                   const double *b, cudaStream_t st) {
+    PINS_TRY(ensure(ws->cgst, sizeof(double) * 8));
+    const bool keep_rows = m <= n;
+    CGSArgs A;
+    memset(&A, 0, sizeof A);
+    A.m = keep_rows ? m : n;
+    A.n = keep_rows ? n : m;
+    const long long *rp = ptr<long long>(ws->rowptr), *cp = ptr<long long>(ws->colptr);
+    const int *ci = ptr<int>(ws->colidx), *ri = ptr<int>(ws->rowidx);
+    const double *v = ptr<double>(ws->val), *vt = ptr<double>(ws->valT);
+    A.rowptr = keep_rows ? rp : cp;
+    A.colidx = keep_rows ? ci : ri;
+    A.val = keep_rows ? v : vt;
+    A.colptr = keep_rows ? cp : rp;
+    A.rowidx = keep_rows ? ri : ci;
+    A.valT = keep_rows ? vt : v;
+    const double *rs = ptr<double>(ws->rowsum), *cs = ptr<double>(ws->colsum);
+    A.dr = keep_rows ? rs : cs;
+    A.dc = keep_rows ? cs : rs;
+    A.mu = mu;
+    A.rhs_r = keep_rows ? rhs : rhs + m;
+    A.rhs_c = keep_rows ? rhs + m : rhs;
+    A.x_r = keep_rows ? x : x + m;
+    A.x_c = keep_rows ? x + m : x;
+    A.rtol = rtol;
+    A.maxit = maxit;
+    if (gradf) {
+        A.grad_r = keep_rows ? gradf : gradg;
+        A.grad_c = keep_rows ? gradg : gradf;
+        A.a_r = keep_rows ? a : b;
+        A.a_c = keep_rows ? b : a;
+    }
+    A.st = ptr<double>(ws->cgst);
+    A.R = (int)((A.m + kCGC - 1) / kCGC);
+    A.Cc = (int)((A.n + kCGC - 1) / kCGC);
+    const size_t smem = kClusterSmem;
+    A.smem = (int)smem;
+    static bool configured = false;
+    if (!configured) {
+        PINS_CUDA(cudaFuncSetAttribute(cg_schur_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        configured = true;
+    }
+    LAUNCH(PINS_PROF_CG, st, cg_schur_cluster_kernel<<<kCGC, kCGT, smem, st>>>(A));
+    PINS_CUDA(cudaGetLastError());
+    return PINS_OK;
+}
+
 double cg_rtol(const pins_params *p, double gnorm) {
     if (p->cg_forcing <= 0.0 || gnorm <= 0.0) return p->cg_tol;
     return std::min(0.5, std::max(p->cg_tol, p->cg_forcing * p->newton_tol / gnorm));
@@ -553,8 +968,6 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
         PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &e));
         *cur = e;
     }
-    PINS_TRY(build_csc(ws, m, n, ptr<long long>(ws->rowptr), ptr<int>(ws->colidx),
-                       ptr<double>(ws->val), ws->nnz, st));
     double *rhs = ptr<double>(ws->rhs);
     LAUNCH(PINS_PROF_VEC, st, scale_concat_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(m, n, pb->eta, ptr<double>(ws->gradf),
                                                               ptr<double>(ws->gradg), rhs));
@@ -562,9 +975,14 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
     const double mu = prm->mu_rel * std::max(cur->maxr, cur->maxc);
     const double rtol = cg_rtol(prm, cur->gnorm);
     double *d = ptr<double>(ws->dir);
-    PINS_TRY(run_cg(ws, m, n, ptr<long long>(ws->rowptr), ptr<int>(ws->colidx), ptr<double>(ws->val),
-                    ptr<double>(ws->rowsum), ptr<double>(ws->colsum), mu, rhs, d, rtol,
-                    prm->cg_maxit, ptr<double>(ws->gradf), ptr<double>(ws->gradg), pb->a, pb->b, st));
+    if (use_cluster_cg(ws, m, n)) {
+        PINS_TRY(run_cg_cluster(ws, m, n, mu, rhs, d, rtol, prm->cg_maxit, ptr<double>(ws->gradf),
+                                ptr<double>(ws->gradg), pb->a, pb->b, st));
+    } else {
+        PINS_TRY(run_cg(ws, m, n, ptr<long long>(ws->rowptr), ptr<int>(ws->colidx), ptr<double>(ws->val),
+                        ptr<double>(ws->rowsum), ptr<double>(ws->colsum), mu, rhs, d, rtol,
+                        prm->cg_maxit, ptr<double>(ws->gradf), ptr<double>(ws->gradg), pb->a, pb->b, st));
+    }
     PINS_CUDA(cudaMemcpyAsync(ws->h + 16, ws->cgst.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
     PINS_CUDA(cudaStreamSynchronize(st));
     const double cg_its = ws->h[16], relres = ws->h[17], slope = ws->h[18], ad = ws->h[19];
@@ -579,7 +997,7 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
             ++trials;
             LAUNCH(PINS_PROF_VEC, st, trial_prep_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(
                 m, n, alpha, 1.0 / pb->eta, f, g, d, ptr<double>(ws->ft), ptr<double>(ws->gt),
-                ptr<double>(ws->eu), ptr<double>(ws->ev)));
+                ptr<double>(ws->eu), ptr<double>(ws->ev), ptr<double>(ws->bu), ptr<double>(ws->bv)));
             PINS_CUDA(cudaGetLastError());
             PINS_TRY(run_eval(ws, pb, phi, psi, s, ptr<double>(ws->ft), ptr<double>(ws->gt), tau, true,
                               st, &e));
@@ -603,27 +1021,6 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
         info[2] = 0.0;
     }
     info[1] = cur->gnorm;
-    return PINS_OK;
-}
-
-int do_sweep(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi,
-             double s, double *f, double *g, cudaStream_t st) {
-    SweepArgs A;
-    A.m = pb->m;
-    A.n = pb->n;
-    A.cd = make_cd(pb);
-    A.phi = phi;
-    A.psi = psi;
-    A.a = pb->a;
-    A.b = pb->b;
-    A.f = f;
-    A.g = g;
-    A.eta = pb->eta;
-    A.inv_eta = 1.0 / pb->eta;
-    A.w = s * pb->cost_scale / pb->eta;
-    PINS_TRY(ensure(ws->tab, sizeof(ExpTable)));
-    A.tab = ptr<ExpTable>(ws->tab);
-    PINS_CUDA(launch_sweep(pb->cost_kind, pb->d, pb->m, pb->n, st, ws->nsm, A));
     return PINS_OK;
 }
 
@@ -738,7 +1135,7 @@ extern "C" int pins_sparsify_dense(pins_workspace *ws, int64_t m, int64_t n, con
     pb.a = ptr<double>(ws->fsave); pb.b = ptr<double>(ws->fsave) + m;
     const double *z = ptr<double>(ws->gsave);
     EvalOut e;
-    PINS_TRY(run_eval(ws, &pb, z, z + m, 1.0, z, z + m, tau, false, st, &e));
+    PINS_TRY(run_eval_legacy(ws, &pb, z, z + m, 1.0, z, z + m, tau, false, st, &e));
     int64_t mm = 0;
     return pins_get_csr(ws, rowptr, colidx, val, cap, nnz_host, &mm);
 }
@@ -832,10 +1229,7 @@ extern "C" int pins_plan(const pins_problem *pb, const double *phi, const double
     return PINS_OK;
 }
 
-extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream) {
-    PINS_TRY(check_problem(pb));
-    PINS_ARG(prm && res && res->f && res->g && res->phi && res->psi, "params / result buffers");
-    PINS_ARG(prm->K >= 1 && prm->T2 >= 0 && prm->T1 >= 0, "budgets");
+static int solve_core(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream) {
     auto t0 = std::chrono::steady_clock::now();
     cudaStream_t st = (cudaStream_t)stream;
     pins_workspace *ws = nullptr;
@@ -867,10 +1261,9 @@ extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_r
         }
         PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &cur));
         int t = 0;
-        while (!(cur.gnorm <= prm->sink_tol) && t < prm->T1) {
-            PINS_TRY(do_sweep(ws, pb, phi, psi, s, f, g, st));
+        if (!(cur.gnorm <= prm->sink_tol) && prm->T1 > 0) {
+            PINS_TRY(sinkhorn_phase(ws, pb, prm, phi, psi, s, f, g, cur.gnorm, &t, st));
             PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &cur));
-            ++t;
         }
         sweeps += t;
         const double g_sink = cur.gnorm;
@@ -991,5 +1384,81 @@ extern "C" int pins_solve_host(const pins_problem *pb_host, const pins_params *p
     PINS_CUDA(e);
     io_bytes_host[0] = h2d;
     io_bytes_host[1] = d2h;
+    return PINS_OK;
+}
+
+// Morton permutation of one point set (pins_order.cuh): perm (device, np)
+static int morton_order(long long np, int d, const double *pts, const double *lohi, int *perm, DevBuf &tmp,
+                        cudaStream_t st) {
+    PINS_TRY(ensure(tmp, sizeof(unsigned long long) * 2 * np + sizeof(int) * np));
+    unsigned long long *k0 = ptr<unsigned long long>(tmp), *k1 = k0 + np;
+    int *i0 = reinterpret_cast<int *>(k1 + np);
+    LAUNCH(PINS_PROF_VEC, st, morton_kernel<<<grid_1d(np, 148), 256, 0, st>>>(np, d, pts, lohi, k0, i0));
+    PINS_CUDA(cudaGetLastError());
+    size_t tb = 0;
+    PINS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, i0, perm, (int)np, 0, 64, st));
+    DevBuf sortmp;
+    PINS_TRY(ensure(sortmp, tb));
+    PINS_CUDA(cub::DeviceRadixSort::SortPairs(sortmp.p, tb, k0, k1, i0, perm, (int)np, 0, 64, st));
+    PINS_CUDA(cudaStreamSynchronize(st));
+    cudaFree(sortmp.p);
+    return PINS_OK;
+}
+
+extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream) {
+    PINS_TRY(check_problem(pb));
+    PINS_ARG(prm && res && res->f && res->g && res->phi && res->psi, "params / result buffers");
+    PINS_ARG(prm->K >= 1 && prm->T2 >= 0 && prm->T1 >= 0, "budgets");
+    auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long m = pb->m, n = pb->n;
+    const bool reorder = pb->cost_kind != PINS_COST_DENSE && (double)m * (double)n >= 65536.0 &&
+                         getenv("PINS_NO_REORDER") == nullptr;
+    if (!reorder) {
+        int rc = solve_core(pb, prm, res, stream);
+        res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return rc;
+    }
+    // permuted copy of the instance (points in Morton order), solve, scatter back
+    const int d = pb->d;
+    DevBuf buf, lohi, tmp;
+    const long long nd = (long long)(m + n) * d + (m + n) + 6 * (m + n);
+    PINS_TRY(ensure(buf, sizeof(double) * nd + sizeof(int) * (m + n)));
+    PINS_TRY(ensure(lohi, sizeof(double) * 32));
+    double *xp = ptr<double>(buf), *yp = xp + m * d, *ap = yp + n * d, *bp = ap + m;
+    double *o = bp + n;                       // 6 (m+n) result slots
+    int *px = reinterpret_cast<int *>(o + 6 * (m + n)), *py = px + m;
+    struct Free {
+        DevBuf *b[3];
+        ~Free() { for (DevBuf *x : b) if (x->p) cudaFree(x->p); }
+    } fr{{&buf, &lohi, &tmp}};
+    LAUNCH(PINS_PROF_VEC, st, bbox_kernel<<<1, 1024, 0, st>>>(m, n, d, pb->x, pb->y, ptr<double>(lohi)));
+    PINS_CUDA(cudaGetLastError());
+    PINS_TRY(morton_order(m, d, pb->x, ptr<double>(lohi), px, tmp, st));
+    PINS_TRY(morton_order(n, d, pb->y, ptr<double>(lohi), py, tmp, st));
+    LAUNCH(PINS_PROF_VEC, st, gather_points_kernel<<<grid_1d(m, 148), 256, 0, st>>>(m, d, px, pb->x, pb->a, xp, ap));
+    LAUNCH(PINS_PROF_VEC, st, gather_points_kernel<<<grid_1d(n, 148), 256, 0, st>>>(n, d, py, pb->y, pb->b, yp, bp));
+    PINS_CUDA(cudaGetLastError());
+    pins_problem q = *pb;
+    q.x = xp; q.y = yp; q.a = ap; q.b = bp;
+    pins_result r = *res;
+    r.f = o; r.g = o + m; r.phi = o + (m + n); r.psi = o + (m + n) + m;
+    r.u = res->u ? o + 2 * (m + n) : nullptr;
+    r.v = res->v ? o + 2 * (m + n) + m : nullptr;
+    PINS_TRY(solve_core(&q, prm, &r, stream));
+    double *const src[6] = {r.f, r.g, r.phi, r.psi, r.u, r.v};
+    double *const dst[6] = {res->f, res->g, res->phi, res->psi, res->u, res->v};
+    for (int t = 0; t < 6; ++t) {
+        if (!src[t] || !dst[t]) continue;
+        const bool rows = (t % 2) == 0;
+        LAUNCH(PINS_PROF_VEC, st, scatter_kernel<<<grid_1d(rows ? m : n, 148), 256, 0, st>>>(
+            rows ? m : n, rows ? px : py, src[t], dst[t]));
+    }
+    PINS_CUDA(cudaGetLastError());
+    PINS_CUDA(cudaStreamSynchronize(st));
+    double *const keep[6] = {res->f, res->g, res->phi, res->psi, res->u, res->v};
+    *res = r;
+    res->f = keep[0]; res->g = keep[1]; res->phi = keep[2]; res->psi = keep[3]; res->u = keep[4]; res->v = keep[5];
+    res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return PINS_OK;
 }

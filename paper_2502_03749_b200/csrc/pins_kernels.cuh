@@ -514,10 +514,19 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     return t;   // valid in thread 0
 }
 
+// sum of the per-block partials, read by warp 0 (lanes stride the blocks,
+// fixed shuffle tree: the same value in every block), broadcast through smem
 __device__ __forceinline__ double grid_reduce(const double *part, int slot, int G) {
-    double t = 0.0;
-    for (int b2 = 0; b2 < G; ++b2) t += part[b2 * 4 + slot];
-    return t;
+    __shared__ double bcast;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = 0.0;
+        for (int b2 = threadIdx.x; b2 < G; b2 += 32) t += __ldcg(part + b2 * 4 + slot);
+        t = warp_sum(t);
+        if (threadIdx.x == 0) bcast = t;
+    }
+    __syncthreads();
+    return bcast;
 }
 
 __global__ void __launch_bounds__(kThreads) cg_kernel(CGArgs A) {
@@ -632,11 +641,13 @@ __global__ void __launch_bounds__(kThreads) cg_kernel(CGArgs A) {
         A.part[blockIdx.x * 4 + 1] = v1;
     }
     grid.sync();
+    const double s0 = grid_reduce(A.part, 0, G);   // every thread: grid_reduce synchronises the block
+    const double s1 = grid_reduce(A.part, 1, G);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         A.st[0] = (double)it;
         A.st[1] = relres;
-        A.st[2] = grid_reduce(A.part, 0, G);
-        A.st[3] = grid_reduce(A.part, 1, G);
+        A.st[2] = s0;
+        A.st[3] = s1;
     }
 }
 
@@ -644,18 +655,23 @@ __global__ void __launch_bounds__(kThreads) cg_kernel(CGArgs A) {
 // small vector kernels
 // =========================================================================
 // trial point (f + alpha df, g + alpha dg) and the separable expm1 factors
+// bu / bv = max(0, -alpha d / eta): X~ at the old point is X~ at the trial point
+// times exp(bu_i + bv_j) at most, which keeps the sum pass's skip test safe for
+// the trial term (pins_pass.cuh)
 __global__ void trial_prep_kernel(long long m, long long n, double alpha, double inv_eta,
                                   const double *f, const double *g, const double *d,
-                                  double *ft, double *gt, double *eu, double *ev) {
+                                  double *ft, double *gt, double *eu, double *ev, double *bu, double *bv) {
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < m + n;
          k += (long long)gridDim.x * blockDim.x) {
         const double dk = alpha * d[k];
         if (k < m) {
             ft[k] = f[k] + dk;
             eu[k] = expm1(-dk * inv_eta);
+            bu[k] = fmax(0.0, -dk * inv_eta);
         } else {
             gt[k - m] = g[k - m] + dk;
             ev[k - m] = expm1(-dk * inv_eta);
+            bv[k - m] = fmax(0.0, -dk * inv_eta);
         }
     }
 }
