@@ -44,7 +44,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BENCH_PARAMS = dict(K=20000, outer_rule=1, outer_tol=1e-7, newton_tol=1e-10)
+# PAPER.md A.2 (lines 477-485) defaults (newton_tol 1e-8, T1, T2, ...) except the outer stop:
+# halving estimator at 1e-7 (reading R6) so the objective meets BASELINE.json's 1e-7 bar
+BENCH_PARAMS = dict(K=20000, outer_rule=1, outer_tol=1e-7, newton_tol=1e-8)
 KKT_TARGET = 1e-8
 OBJ_RTOL = 1e-7
 
@@ -108,35 +110,54 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ work model
-def algorithmic_work(cls: str, w) -> dict:
-    """Algorithmic work of ONE launch of a dense-pass kernel class.
+def kernel_roofline(cls: str, w, launches: int, ms: float, clocks_mhz: float, peaks: dict, counts: dict) -> dict:
+    """Roofline entry for one kernel class (DESIGN.md §7 gives every number used here).
 
-    Dense passes touch every (i, j) of the m x n block once.  For point costs
-    there is no m x n operand in HBM (the cost is recomputed from the m + n
-    points), so the pass is bound by the fp64 pipe: the exponential of
-    Eq. (7) per entry.  For a dense cost the operand C is read once per pass
-    (8 bytes per entry): HBM bound."""
-    mn = float(w.m) * float(w.n)
-    if w.kind == 0:
-        return {"bound": "hbm", "unit": "GB/s", "per_launch": 8.0 * mn, "what": "8 B of C per entry"}
-    return {"bound": "alu", "unit": "Gexp/s", "per_launch": mn, "what": "one fp64 exp (Eq. (7)) per entry"}
-
-
-def alu_peak_gexp(sm_mhz: float) -> float:
-    """fp64-pipe roofline of the point-cost dense passes, in entries (exps) per second.
-
-    B200: 148 SMs x 64 fp64 lanes per clock.  The minimal fp64 work of one entry
-    of a sweep / eval pass is FP64_OPS_PER_ENTRY pipe operations (exp: range
-    reduction 3, degree-6 polynomial 6, reconstruction 2; the exponent
-    z = R + S - w D: 1; the accumulation: 1).  Peak = lanes*clock / ops."""
-    FP64_OPS_PER_ENTRY = 13.0
-    return 148 * 64 * sm_mhz * 1e6 / FP64_OPS_PER_ENTRY / 1e9
+    sweep_row / eval (dense passes over the m x n block):
+      dense cost  -> "hbm": 8 B of C read per entry and pass, peak = measured HBM copy GB/s.
+      point cost  -> "alu": minimal SM issue work per entry = d FFMA (x.y) + 3 (norm
+                    combine, exponent, skip test); peak = 148 SM x 4 warp-instr/clk x
+                    32 lanes x clock / (d + 3)  entries/s.  The work is m*n entries per
+                    half-sweep (sweep_row launches are half-sweeps) and 2*m*n per eval
+                    (both orientations in one launch).
+    cg (cluster CG, one launch per Newton step): "hbm" bytes = per iteration
+      (CSR + CSC: 2 x 12 B x nnz) + 8 vectors x 8 B x (m + n), x iterations; peak = HBM.
+      (Its working set is on-chip; the fraction shows how latency-bound it is.)"""
+    avg_s = ms / max(1, launches) / 1e3
+    if cls in ("sweep_row", "eval"):
+        mult = 1.0 if cls == "sweep_row" else 2.0
+        entries = mult * float(w.m) * float(w.n)
+        if w.kind == 0:
+            ach = 8.0 * entries / avg_s / 1e9
+            peak = peaks.get("hbm_gbs", 6650.0)
+            return {"kernel": cls, "bound": "hbm", "unit": "GB/s", "achieved": ach, "peak": peak,
+                    "frac": ach / peak, "work_per_launch": f"{8 * entries:.3g} B (8 B/entry)",
+                    "peak_source": "measured" if "hbm_gbs" in peaks else "fallback"}
+        d = w.X.shape[1]
+        ach = entries / avg_s / 1e9
+        peak = 148 * 4 * 32 * clocks_mhz * 1e6 / (d + 3) / 1e9
+        return {"kernel": cls, "bound": "alu", "unit": "Gentries/s", "achieved": ach, "peak": peak,
+                "frac": ach / peak, "work_per_launch": f"{entries:.3g} entries",
+                "peak_source": f"derived: 148 SM x 4 issue x 32 lanes x {clocks_mhz:.0f} MHz / (d+3={d + 3}) instr per entry"}
+    if cls == "cg":
+        its = counts.get("cg_iters", 0) / max(1, counts.get("newton_iters", 1))
+        nnz = counts.get("nnz_late", 2 * (w.m + w.n))
+        byts = its * (24.0 * nnz + 64.0 * (w.m + w.n))
+        ach = byts / avg_s / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        return {"kernel": cls, "bound": "hbm", "unit": "GB/s", "achieved": ach, "peak": peak, "frac": ach / peak,
+                "work_per_launch": f"{byts:.3g} B ({its:.0f} it x (24 B x nnz {nnz} + 64 B x (m+n)))",
+                "peak_source": "measured" if "hbm_gbs" in peaks else "fallback"}
+    return {"kernel": cls}
 
 
 # ------------------------------------------------------------ cpu baseline
-def oracle_rates(w, budget_s: float):
-    """Time the oracle's own operations on the FULL instance (bounded: one call
-    each, stops early when the budget is spent).  Returns seconds per op."""
+def oracle_rates(w, budget_s: float, cg_per_newton: float):
+    """Time the oracle's own operations, as they stand, on the FULL instance at
+    the first subproblem (k = 0, X^0 = a b^T): one Sinkhorn sweep, one residual
+    evaluation, and one Newton direction with 20 and with 40 CG iterations (the
+    difference gives the per-CG-iteration cost), plus one line-search trial.
+    Returns seconds per operation."""
     import numpy as np
     from oracle import pins_oracle as po
     t0 = time.time()
@@ -152,28 +173,39 @@ def oracle_rates(w, budget_s: float):
     t0 = time.time()
     po.residual_l1(f, g, Ck, w.a, w.b, w.eta)
     t_eval = time.time() - t0
-    t_newton = None
     spent = t_cost + t_sweep + t_eval
-    if spent + 4 * t_eval < budget_s:
-        prm = po.Params(eta=w.eta)
+    out = dict(sweep=t_sweep, eval=t_eval, cost=t_cost)
+    if spent + 6 * t_eval < budget_s:
+        ts = []
+        for its in (20, 40):
+            prm = po.Params(eta=w.eta, cg_tol=0.0, cg_forcing=0.0, cg_maxit=its)
+            t0 = time.time()
+            df, dg, _ = po.newton_direction(f, g, Ck, w.a, w.b, w.eta, prm)
+            ts.append(time.time() - t0)
+        per_it = max(0.0, (ts[1] - ts[0]) / 20.0)
         t0 = time.time()
-        po.newton_step(f, g, Ck, w.a, w.b, w.eta, prm)
-        t_newton = time.time() - t0
-    if t_newton is None:
-        t_newton = 4 * t_eval      # plan + sparsify + one line-search trial, lower bound
-    return dict(sweep=t_sweep, eval=t_eval, newton=t_newton, cost=t_cost)
+        po.dual_increase(f, g, df, dg, 1.0, Ck, w.a, w.b, w.eta)
+        t_ls = time.time() - t0
+        out["newton"] = max(0.0, ts[0] - 20 * per_it) + per_it * cg_per_newton + t_ls
+        out["cg_it"] = per_it
+    else:
+        out["newton"] = 4 * t_eval      # plan + sparsify + one line-search trial, lower bound
+        out["cg_it"] = None
+    return out
 
 
 def cpu_baseline(w, counts: dict, budget_s: float, cores: int):
-    r = oracle_rates(w, budget_s)
     outer, sweeps, newton = counts["outer_iters"], counts["sweeps"], counts["newton_iters"]
-    # oracle PINS per outer iteration: one shifted cost + one residual, per sweep a
-    # sweep + a residual, per Newton step a step + a residual, plus the centre update
-    est = (outer * (r["cost"] * 0 + r["eval"] * 2) + sweeps * (r["sweep"] + r["eval"])
-           + newton * (r["newton"] + r["eval"]))
-    sample = (f"oracle fp64 numpy on the full {w.m}x{w.n} instance: one Sinkhorn sweep "
-              f"{r['sweep']:.2f}s, one residual {r['eval']:.2f}s, one Newton step {r['newton']:.2f}s, "
-              f"scaled by {outer} outer / {sweeps} sweeps / {newton} Newton steps per solve")
+    cgpn = counts["cg_iters"] / max(1, newton)
+    r = oracle_rates(w, budget_s, cgpn)
+    # oracle PINS per outer iteration: one residual (+ the objective), per sweep a
+    # sweep + a residual, per Newton step a step + a residual
+    est = outer * 2 * r["eval"] + sweeps * (r["sweep"] + r["eval"]) + newton * (r["newton"] + r["eval"])
+    cg_txt = f", {r['cg_it'] * 1e3:.1f} ms per CG iteration" if r.get("cg_it") is not None else ""
+    sample = (f"oracle fp64 numpy, full {w.m}x{w.n} instance at k=0: one Sinkhorn sweep "
+              f"{r['sweep']:.2f}s, one residual {r['eval']:.2f}s, one Newton step {r['newton']:.2f}s"
+              f"{cg_txt}; scaled by this solve's {outer} outer / {sweeps} sweeps / {newton} Newton steps "
+              f"/ {cgpn:.0f} CG iterations per Newton step")
     return {"value": est, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample}
 
 
@@ -303,26 +335,19 @@ def main():
     if rank == 0:
         r0 = results[-1]
         counts = {k: r0[k] for k in ("outer_iters", "sweeps", "newton_iters", "cg_iters")}
-        dense = {c: prof[c] for c in ("sweep_row", "sweep_col", "eval")}
-        dom = max(dense, key=lambda c: dense[c]["ms"])
-        total_ms = sum(v["ms"] for v in prof.values())
-        L = max(1, dense[dom]["launches"])
-        avg_ms = dense[dom]["ms"] / L
-        wk = algorithmic_work(dom, w)
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
             if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-        if wk["bound"] == "hbm":
-            achieved = wk["per_launch"] / (avg_ms * 1e-3) / 1e9
-            peak = peaks.get("hbm_gbs", 6650.0)
-            peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-        else:
-            achieved = wk["per_launch"] / (avg_ms * 1e-3) / 1e9
-            peak = alu_peak_gexp(clocks["sm_mhz"] or 1965.0)
-            peak_src = "derived: 148 SM x 64 fp64 lanes x sm clock / 13 fp64 ops per entry (DESIGN.md §7)"
-        roof = {"bound": wk["bound"], "kernel": dom, "achieved": achieved, "peak": peak, "unit": wk["unit"],
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                "launches": dense[dom]["launches"], "avg_launch_us": avg_ms * 1e3,
-                "share_of_device_time": dense[dom]["ms"] / max(total_ms, 1e-9), "work": wk["what"]}
+        total_ms = sum(v["ms"] for v in prof.values())
+        mhz = clocks["sm_mhz"] or 1965.0
+        kerns = {}
+        for c in ("sweep_row", "eval", "cg"):
+            if prof[c]["launches"]:
+                e = kernel_roofline(c, w, prof[c]["launches"], prof[c]["ms"], mhz, peaks, counts)
+                e.update(launches=prof[c]["launches"], avg_launch_us=prof[c]["ms"] / prof[c]["launches"] * 1e3,
+                         share_of_device_time=prof[c]["ms"] / max(total_ms, 1e-9), traffic=None)
+                kerns[c] = e
+        dom = max(kerns, key=lambda c: kerns[c]["share_of_device_time"])
+        roof = dict(kerns[dom])
         launches = int(sum(v["launches"] for v in prof.values()))
         line = {
             "metric": "s to KKT<1e-8 (n=10k, c3_gmm10k)", "value": value, "unit": "s",
@@ -339,6 +364,7 @@ def main():
             "counts": counts,
             "clocks": clocks,
             "roofline": roof,
+            "roofline_kernels": kerns,
             "prof": {c: {"launches": v["launches"], "ms_per_step": v["ms"] / args.steps} for c, v in prof.items()},
             "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": "s", "h2d_bytes_per_step": io[0], "d2h_bytes_per_step": io[1]},

@@ -1,0 +1,31 @@
+"""Short, deterministic targets for `ncu --set full` (one kernel family per mode).
+
+    python tools/ncu_target.py sweep|eval|cg [config]
+sweep: 30 Sinkhorn sweeps from X^0 (lse_pass_kernel); eval: 10 evaluations with
+sparsify (sum_pass_kernel); cg: a PINS solve capped at 10 outer iterations
+(cg_schur_cluster_kernel from the 6th on).  Inputs: the seeded workload.
+"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2502_03749_b200 import pins
+from workloads import make
+
+mode = sys.argv[1]
+name = sys.argv[2] if len(sys.argv) > 2 else "c3_gmm10k"
+w = make(name)
+pb = pins.DeviceProblem.from_workload(w)
+if mode in ("sweep", "eval"):
+    phi, psi, s = pins.center_init(pb)
+    f = torch.zeros(w.m, dtype=torch.float64, device="cuda")
+    g = torch.zeros(w.n, dtype=torch.float64, device="cuda")
+    ws = pins.Workspace()
+    for _ in range(30 if mode == "sweep" else 20):
+        pins.sinkhorn_sweep(ws, pb, phi, psi, s, f, g)
+    if mode == "eval":
+        for _ in range(10):
+            pins.evaluate(ws, pb, phi, psi, s, f, g, tau=1e-4 / (w.m * w.n))
+else:
+    r = pins.solve(pb, pins.default_params(K=10, outer_tol=0.0, newton_tol=1e-8))
+torch.cuda.synchronize()
+print("ok", mode, name)
