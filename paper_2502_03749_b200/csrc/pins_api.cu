@@ -147,7 +147,7 @@ struct pins_workspace {
     DevBuf cgvec, cgpart, cgst, st, ft, gt, eu, ev, bu, bv, dir, rhs, tab, fsave, gsave, uv;
     // v2 dense passes
     SideBufs sb[2];
-    DevBuf x32, y32, x64, y64, nx32, ny32, pinfo, ctl, gticket, pst, tol;
+    DevBuf x32, y32, x64, y64, nx32, ny32, xh, yh, pinfo, ctl, gticket, pst, tol;
     const void *key_C = nullptr, *key_x = nullptr, *key_y = nullptr;
     long long key_m = -1, key_n = -1, key_ldc = -1;
     int key_kind = -1, key_d = -1;
@@ -205,7 +205,7 @@ extern "C" void pins_workspace_destroy(pins_workspace *ws) {
                       &ws->colcnt, &ws->colptr, &ws->cursor, &ws->rowidx, &ws->valT, &ws->cgvec,
                       &ws->cgpart, &ws->cgst, &ws->st, &ws->ft, &ws->gt, &ws->eu, &ws->ev,
                       &ws->dir, &ws->rhs, &ws->tab, &ws->fsave, &ws->gsave, &ws->uv, &ws->bu, &ws->bv,
-                      &ws->x32, &ws->y32, &ws->x64, &ws->y64, &ws->nx32, &ws->ny32, &ws->pinfo,
+                      &ws->x32, &ws->y32, &ws->x64, &ws->y64, &ws->nx32, &ws->ny32, &ws->xh, &ws->yh, &ws->pinfo,
                       &ws->ctl, &ws->gticket, &ws->pst, &ws->tol};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
@@ -562,6 +562,17 @@ int prepare_pass(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
             const double bound = (std::sqrt(nxm) + std::sqrt(nym)) * (std::sqrt(nxm) + std::sqrt(nym));
             exact32 = integral && bound < two24 && ax < two24 && ay < two24;
             ws->cost_row = ws->cost_col = exact32 ? PC_SQ32 : PC_SQ64;
+            // tensor cores: fp16 operands exact for integers |x| <= 2048, d <= 16
+            if (exact32 && std::max(ax, ay) <= 2048.0 && pb->d <= 16 && getenv("PINS_NO_TC") == nullptr) {
+                PINS_TRY(ensure(ws->xh, sizeof(__half) * m * 16));
+                PINS_TRY(ensure(ws->yh, sizeof(__half) * n * 16));
+                LAUNCH(PINS_PROF_VEC, st, to_half16_kernel<<<grid_1d(m * 16, ws->nsm), 256, 0, st>>>(
+                    m, dp, ptr<float>(ws->x32), ptr<__half>(ws->xh)));
+                LAUNCH(PINS_PROF_VEC, st, to_half16_kernel<<<grid_1d(n * 16, ws->nsm), 256, 0, st>>>(
+                    n, dp, ptr<float>(ws->y32), ptr<__half>(ws->yh)));
+                PINS_CUDA(cudaGetLastError());
+                ws->cost_row = ws->cost_col = PC_SQTC;
+            }
         } else {
             exact32 = integral && 2.0 * pb->d * std::max(ax, ay) < two24;
             ws->cost_row = ws->cost_col = exact32 ? PC_L132 : PC_L164;
@@ -590,6 +601,8 @@ void fill_side(pins_workspace *ws, const pins_problem *pb, int o, const double *
     P.nyc = ptr<float>(row ? ws->ny32 : ws->nx32);
     P.xr64 = ptr<double>(row ? ws->x64 : ws->y64);
     P.yc64 = ptr<double>(row ? ws->y64 : ws->x64);
+    P.xrh = ptr<__half>(row ? ws->xh : ws->yh);
+    P.ych = ptr<__half>(row ? ws->yh : ws->xh);
     P.fr = row ? f : g;
     P.phir = row ? phi : psi;
     P.gc = row ? g : f;
@@ -634,6 +647,7 @@ cudaError_t launch_lse(int cost, int dp, int grid, cudaStream_t st, const PassAr
         case PC_SQ32: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_SQ32, DP><<<grid, kPT, 0, st>>>(A))); break;
         case PC_L132: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_L132, DP><<<grid, kPT, 0, st>>>(A))); break;
         case PC_SQ64: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_SQ64, DP><<<grid, kPT, 0, st>>>(A))); break;
+        case PC_SQTC: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_SQTC, DP><<<grid, kPT, 0, st>>>(A))); break;
         default: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_L164, DP><<<grid, kPT, 0, st>>>(A))); break;
     }
     return cudaGetLastError();
@@ -645,6 +659,7 @@ cudaError_t launch_sum(int cost, int dp, int grid, cudaStream_t st, const PassAr
         case PC_SQ32: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_SQ32, PC_SQ32, DP><<<grid, kPT, 0, st>>>(A))); break;
         case PC_L132: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_L132, PC_L132, DP><<<grid, kPT, 0, st>>>(A))); break;
         case PC_SQ64: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_SQ64, PC_SQ64, DP><<<grid, kPT, 0, st>>>(A))); break;
+        case PC_SQTC: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_SQTC, PC_SQTC, DP><<<grid, kPT, 0, st>>>(A))); break;
         default: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_L164, PC_L164, DP><<<grid, kPT, 0, st>>>(A))); break;
     }
     return cudaGetLastError();

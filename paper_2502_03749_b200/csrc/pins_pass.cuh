@@ -32,6 +32,9 @@
 // scalars merged in block order by the last row block of the launch.
 #pragma once
 #include "pins_device.cuh"
+#include "pins_tc.cuh"
+
+#include <type_traits>
 
 namespace pins {
 
@@ -48,6 +51,7 @@ enum : int {
     PC_L132 = 3,        // integer points, exact in fp32: D = sum |x - y|
     PC_SQ64 = 4,        // generic points, fp64: D = sum (x - y)^2
     PC_L164 = 5,        // generic points, fp64: D = sum |x - y|
+    PC_SQTC = 6,        // integer points |x| <= 2048: x.y on the tensor cores (tcgen05, fp16 exact)
 };
 
 struct PassSide {
@@ -60,6 +64,7 @@ struct PassSide {
     const float *xr32, *yc32;       // fp32 points, M x dp / N x dp (zero padded)
     const float *nxr, *nyc;         // squared norms (PC_SQ32)
     const double *xr64, *yc64;      // fp64 points, M x dp / N x dp (zero padded)
+    const __half *xrh, *ych;        // PC_SQTC: fp16 points, M x 16 / N x 16 (zero padded)
     // potentials: pass-row side (fr + phir), pass-column side (gc + psic)
     const double *fr, *phir, *gc, *psic;
     int m1_row;                     // SUM: the "-1" of Eq. (7) sits on the pass-row potential
@@ -113,48 +118,127 @@ __device__ __forceinline__ double pot_p(double f, double phi, double inv_eta) {
 }
 
 // ---------------------------------------------------------------- staging
-// Per chunk: kCC pass columns j0 .. j0+kCC-1 (tail-padded).
+// Chunks of kCC pass columns, double-buffered in shared memory (single-buffered
+// for the dense row orientation, whose 128 x kCC tile is large).  Each thread
+// prefetches its share of chunk c+2 into registers while chunk c is computed
+// (Pref), and stores it into the free buffer at the next chunk boundary.
 template <int COST, int DP>
-struct Stage {
-    static constexpr int NY32 = (COST == PC_SQ32 || COST == PC_L132) ? kCC * DP : 4;
-    static constexpr int NY64 = (COST == PC_SQ64 || COST == PC_L164) ? kCC * DP : 1;
-    static constexpr int NT = (COST == PC_DENSE_ROW) ? kCC * (kPT + 1) : 1;
-    double q[kCC];                  // column potential
-    double ev[kCC], bv[kCC];        // trial factors / bumps
-    double y64[NY64];               // fp64 points
-    double tile[NT];                // dense row orientation: C[i0 + r][j0 + c] -> tile[c * (kPT+1) + r]
-    alignas(16) float y32[NY32];    // fp32 points
+struct Buf {
+    static constexpr bool PTS32 = COST == PC_SQ32 || COST == PC_L132;
+    static constexpr bool PTS64 = COST == PC_SQ64 || COST == PC_L164;
+    double q[kCC];                               // column potential
+    double qt[kCC];                              // skip-test column value (q + trial bump)
+    double ev[kCC];                              // trial factor
     float ny[kCC];
+    alignas(16) float y32[PTS32 ? kCC * DP : 4];
+    double y64[PTS64 ? kCC * DP : 1];
+    alignas(128) unsigned char yh[COST == PC_SQTC ? kCC * 32 : 16];   // UMMA B tile (kCC x 16 fp16)
+    double tile[COST == PC_DENSE_ROW ? kCC * (kPT + 1) : 1];
 };
 
+template <int COST>
+constexpr int kNBuf = COST == PC_DENSE_ROW ? 1 : 2;
+
 template <int COST, int DP>
-__device__ __forceinline__ void stage_cost(Stage<COST, DP> &sg, const PassSide &P, long long i0, long long j0,
-                                           int nc) {
-    const int tid = threadIdx.x;
-    if constexpr (COST == PC_SQ32 || COST == PC_L132) {
-        for (int t = tid; t < kCC * DP; t += kPT) {
-            const int c = t / DP;
-            sg.y32[t] = (c < nc) ? P.yc32[(j0 + c) * DP + (t - c * DP)] : 0.f;
+struct Pref {
+    static constexpr bool PTS32 = COST == PC_SQ32 || COST == PC_L132;
+    static constexpr bool PTS64 = COST == PC_SQ64 || COST == PC_L164;
+    static constexpr int NY = (PTS32 || PTS64) ? (kCC * DP + kPT - 1) / kPT : 1;
+    double g, psi, ev, bv;
+    float ny;
+    float y32[PTS32 ? NY : 1];
+    double y64[PTS64 ? NY : 1];
+    uint2 yh;
+    // global -> registers (this thread's share of columns j0 .. j0+nc-1)
+    __device__ __forceinline__ void load(const PassSide &P, long long j0, int nc, bool trial) {
+        const int tid = threadIdx.x;
+        if (tid < kCC) {
+            const bool ok = tid < nc;
+            g = ok ? P.gc[j0 + tid] : 0.0;
+            psi = ok ? P.psic[j0 + tid] : 0.0;
+        } else if (tid < 2 * kCC && trial) {
+            const int c = tid - kCC;
+            const bool ok = c < nc;
+            ev = ok ? P.ev[j0 + c] : 0.0;
+            bv = ok ? P.bv[j0 + c] : 0.0;
         }
-        if (COST == PC_SQ32)
-            for (int c = tid; c < kCC; c += kPT) sg.ny[c] = (c < nc) ? P.nyc[j0 + c] : 0.f;
-    } else if constexpr (COST == PC_SQ64 || COST == PC_L164) {
-        for (int t = tid; t < kCC * DP; t += kPT) {
-            const int c = t / DP;
-            sg.y64[t] = (c < nc) ? P.yc64[(j0 + c) * DP + (t - c * DP)] : 0.0;
+        if (COST == PC_SQ32 && tid >= 2 * kCC && tid < 3 * kCC) {
+            const int c = tid - 2 * kCC;
+            ny = c < nc ? P.nyc[j0 + c] : 0.f;
         }
-    } else if constexpr (COST == PC_DENSE_ROW) {
-        // rows i0 .. i0+kPT-1 of C, columns j0 .. j0+kCC-1: warp w loads rows w, w+4, ...;
-        // lane = column (coalesced 256 B per row); stored transposed with a pad column
-        const int lane = tid & 31, warp = tid >> 5;
-        const long long rows = P.M - i0;
-        for (int r = warp; r < kPT; r += kPT / 32) {
-            double v = 0.0;
-            if (r < rows && lane < nc) v = __ldg(P.C + (i0 + r) * P.ldc + j0 + lane);
-            sg.tile[lane * (kPT + 1) + r] = v;
+        if constexpr (PTS32) {
+#pragma unroll
+            for (int q = 0; q < NY; ++q) {
+                const int t = tid + q * kPT;
+                const int c = t / DP;
+                y32[q] = (t < kCC * DP && c < nc) ? P.yc32[(j0 + c) * DP + (t - c * DP)] : 0.f;
+            }
+        } else if constexpr (PTS64) {
+#pragma unroll
+            for (int q = 0; q < NY; ++q) {
+                const int t = tid + q * kPT;
+                const int c = t / DP;
+                y64[q] = (t < kCC * DP && c < nc) ? P.yc64[(j0 + c) * DP + (t - c * DP)] : 0.0;
+            }
+        } else if constexpr (COST == PC_SQTC) {
+            const int c = tid >> 2, kq = (tid & 3) * 4;     // 4 fp16 of column c per thread
+            yh = (c < nc) ? *reinterpret_cast<const uint2 *>(P.ych + (j0 + c) * 16 + kq) : make_uint2(0u, 0u);
+            if (tid >= 2 * kCC && tid < 3 * kCC) {
+                const int cc = tid - 2 * kCC;
+                ny = cc < nc ? P.nyc[j0 + cc] : 0.f;
+            }
         }
     }
-}
+    // registers -> shared buffer.  qmode: 0 q = (g+psi)/eta, 1 q = (g+psi)/eta - 1
+    __device__ __forceinline__ void store(Buf<COST, DP> &B, const PassSide &P, long long i0, long long j0, int nc,
+                                          double inv_eta, int qmode, bool trial) {
+        const int tid = threadIdx.x;
+        if (tid < kCC) {
+            double q = -INFINITY;
+            if (tid < nc) q = qmode ? pot_p(g, psi, inv_eta) : pot_q(g, psi, inv_eta);
+            B.q[tid] = q;
+            if (!trial) B.qt[tid] = q;
+        } else if (tid < 2 * kCC && trial) {
+            B.ev[tid - kCC] = ev;
+        }
+        if (COST == PC_SQ32 || COST == PC_SQTC)
+            if (tid >= 2 * kCC && tid < 3 * kCC) B.ny[tid - 2 * kCC] = ny;
+        if constexpr (PTS32) {
+#pragma unroll
+            for (int q = 0; q < NY; ++q) {
+                const int t = tid + q * kPT;
+                if (t < kCC * DP) B.y32[t] = y32[q];
+            }
+        } else if constexpr (PTS64) {
+#pragma unroll
+            for (int q = 0; q < NY; ++q) {
+                const int t = tid + q * kPT;
+                if (t < kCC * DP) B.y64[t] = y64[q];
+            }
+        } else if constexpr (COST == PC_SQTC) {
+            const int c = tid >> 2, kq = (tid & 3) * 4;
+            *reinterpret_cast<uint2 *>(B.yh + tc::kmajor_off(c, kq)) = yh;
+        } else if constexpr (COST == PC_DENSE_ROW) {
+            // rows i0 .. i0+kPT-1 of C, columns j0 .. j0+kCC-1: warp w loads rows w, w+4, ...;
+            // lane = column (coalesced 256 B per row); stored transposed with a pad column
+            const int lane = tid & 31, warp = tid >> 5;
+            const long long rows = P.M - i0;
+            for (int r = warp; r < kPT; r += kPT / 32) {
+                double v = 0.0;
+                if (r < rows && lane < nc) v = __ldg(P.C + (i0 + r) * P.ldc + j0 + lane);
+                B.tile[lane * (kPT + 1) + r] = v;
+            }
+        }
+    }
+    // trial: the skip-test value q + bv needs q, written by threads < kCC
+    __device__ __forceinline__ void store_trial_qt(Buf<COST, DP> &B) {
+        const int tid = threadIdx.x;
+        if (tid >= kCC && tid < 2 * kCC) {
+            const int c = tid - kCC;
+            B.qt[c] = B.q[c] + bv;
+        }
+    }
+};
 
 // distance of the thread's pass row to staged column c (as fp64)
 template <int COST, int DP>
@@ -163,17 +247,16 @@ struct RowPt {
     float nx;
     double x64[DP > 0 ? DP : 1];
     __device__ __forceinline__ void load(const PassSide &P, long long i, bool valid) {
-        if constexpr (COST == PC_SQ32 || COST == PC_L132) {
+        if constexpr (COST == PC_SQ32 || COST == PC_L132 || COST == PC_SQTC) {
 #pragma unroll
             for (int k = 0; k < DP; ++k) x32[k] = valid ? P.xr32[i * DP + k] : 0.f;
-            nx = (COST == PC_SQ32 && valid) ? P.nxr[i] : 0.f;
+            nx = ((COST == PC_SQ32 || COST == PC_SQTC) && valid) ? P.nxr[i] : 0.f;
         } else if constexpr (COST == PC_SQ64 || COST == PC_L164) {
 #pragma unroll
             for (int k = 0; k < DP; ++k) x64[k] = valid ? P.xr64[i * DP + k] : 0.0;
         }
     }
-    // D(i, j) from the staged chunk (points kinds)
-    __device__ __forceinline__ double dist(const Stage<COST, DP> &sg, int c) const {
+    __device__ __forceinline__ double dist(const Buf<COST, DP> &sg, int c) const {
         if constexpr (COST == PC_SQ32) {
             const float4 *yv = reinterpret_cast<const float4 *>(sg.y32 + c * DP);
             float dot = 0.f;
@@ -223,7 +306,7 @@ __device__ __forceinline__ double dist_global(const PassSide &P, const RowPt<COS
                                               long long j) {
     if constexpr (COST == PC_DENSE_ROW) return P.C[i * P.ldc + j];
     else if constexpr (COST == PC_DENSE_COL) return P.C[j * P.ldc + i];
-    else if constexpr (COST == PC_SQ32) {
+    else if constexpr (COST == PC_SQ32 || COST == PC_SQTC) {
         float dot = 0.f;
 #pragma unroll
         for (int k = 0; k < DP; ++k) dot = fmaf(rp.x32[k], P.yc32[j * DP + k], dot);
@@ -249,13 +332,112 @@ __device__ __forceinline__ double dist_global(const PassSide &P, const RowPt<COS
     }
 }
 
-template <int COST, int DP>
-__device__ __forceinline__ double chunk_dist(const Stage<COST, DP> &sg, const PassSide &P,
-                                             const RowPt<COST, DP> &rp, long long i, long long j, int c,
-                                             bool valid) {
-    if constexpr (COST == PC_DENSE_ROW) return sg.tile[c * (kPT + 1) + threadIdx.x];
-    else if constexpr (COST == PC_DENSE_COL) return valid ? __ldg(P.C + j * P.ldc + i) : 0.0;
-    else return rp.dist(sg, c);
+// Tensor-core state of a CTA (PC_SQTC): A tile (the CTA's 128 pass rows as
+// fp16, UMMA K-major), TMEM double buffer of kCC fp32 columns, two mbarriers.
+template <int AH>
+struct TcStateT {
+    alignas(128) unsigned char ah[AH];
+    uint64_t mbar[2];
+    uint32_t tbase;
+};
+using TcState = TcStateT<kPT * 32>;
+template <int COST>
+using TcFor = typename std::conditional<COST == PC_SQTC, TcState, TcStateT<16>>::type;
+
+// Streams the column range [jb, je) through the staging buffers and calls
+// body(c0, nc, buf, dots) per chunk: for PC_SQTC `dots` holds this thread's
+// kCC dot products x_i.y_j from TMEM; for the other costs it is unused.
+template <int COST, int DP, class TS, class Body>
+__device__ __forceinline__ void stream_columns(const PassSide &P, long long i0, long long jb, long long je,
+                                               double inv_eta, int qmode, bool trial, Buf<COST, DP> *bufs,
+                                               TS *tcs, Body body) {
+    constexpr int NB = kNBuf<COST>;
+    const long long nch = (je - jb + kCC - 1) / kCC;
+    if (nch <= 0) return;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    Pref<COST, DP> pf;
+    constexpr uint32_t idesc = tc::make_idesc(kCC);
+    auto nc_of = [&](long long c) { return (int)min((long long)kCC, je - (jb + c * kCC)); };
+    // prologue: chunk 0 into buffer 0, prefetch chunk 1
+    pf.load(P, jb, nc_of(0), trial);
+    pf.store(bufs[0], P, i0, jb, nc_of(0), inv_eta, qmode, trial);
+    if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0]); }
+    if (NB > 1 && nch > 1) pf.load(P, jb + kCC, nc_of(1), trial);
+    if constexpr (COST == PC_SQTC) tc::fence_proxy_async();
+    __syncthreads();
+    if constexpr (COST == PC_SQTC) {
+        if (tid == 0) {
+            tc::fence_after();
+            tc::mma_f16(tcs->tbase, tc::make_desc(tcs->ah), tc::make_desc(bufs[0].yh), idesc);
+            tc::commit(&tcs->mbar[0]);
+        }
+    }
+    for (long long c = 0; c < nch; ++c) {
+        const int cur = NB > 1 ? (int)(c & 1) : 0;
+        if (NB > 1 && c + 1 < nch) {
+            const int nxt = cur ^ 1;
+            if constexpr (COST == PC_SQTC) tc::fence_before();
+            __syncthreads();                         // chunk c-1 fully consumed
+            pf.store(bufs[nxt], P, i0, jb + (c + 1) * kCC, nc_of(c + 1), inv_eta, qmode, trial);
+            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[nxt]); }
+            if (c + 2 < nch) pf.load(P, jb + (c + 2) * kCC, nc_of(c + 2), trial);
+            if constexpr (COST == PC_SQTC) tc::fence_proxy_async();
+            __syncthreads();
+            if constexpr (COST == PC_SQTC) {
+                if (tid == 0) {
+                    tc::fence_after();
+                    tc::mma_f16(tcs->tbase + nxt * kCC, tc::make_desc(tcs->ah), tc::make_desc(bufs[nxt].yh), idesc);
+                    tc::commit(&tcs->mbar[nxt]);
+                }
+            }
+        } else if (NB == 1 && c > 0) {
+            __syncthreads();
+            pf.load(P, jb + c * kCC, nc_of(c), trial);
+            pf.store(bufs[0], P, i0, jb + c * kCC, nc_of(c), inv_eta, qmode, trial);
+            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0]); }
+            __syncthreads();
+        }
+        float dots[COST == PC_SQTC ? kCC : 1];
+        if constexpr (COST == PC_SQTC) {
+            tc::mbar_wait(&tcs->mbar[cur], (uint32_t)((c >> 1) & 1));
+            tc::fence_after();
+            tc::ld32(tcs->tbase + ((uint32_t)(32 * (warp & 3)) << 16) + cur * kCC, dots);
+        }
+        body(jb + c * kCC, nc_of(c), bufs[cur], dots);
+    }
+}
+
+// CTA-level tensor-core setup / teardown (PC_SQTC only)
+template <class TS>
+__device__ __forceinline__ void tc_setup(TS &T, const PassSide &P, long long i0) {
+    const int tid = threadIdx.x;
+    const long long i = i0 + tid;
+    uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
+    if (i < P.M) {
+        lo = *reinterpret_cast<const uint4 *>(P.xrh + i * 16);
+        hi = *reinterpret_cast<const uint4 *>(P.xrh + i * 16 + 8);
+    }
+    *reinterpret_cast<uint4 *>(T.ah + tc::kmajor_off(tid, 0)) = lo;
+    *reinterpret_cast<uint4 *>(T.ah + tc::kmajor_off(tid, 8)) = hi;
+    if (tid < 32) tc::tmem_alloc(&T.tbase, 2 * kCC);
+    if (tid == 0) {
+        tc::mbar_init(&T.mbar[0], 1);
+        tc::mbar_init(&T.mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+}
+template <class TS>
+__device__ __forceinline__ void tc_teardown(TS &T) {
+    tc::fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        tc::fence_after();
+        tc::tmem_free(T.tbase, 2 * kCC);
+    }
 }
 
 // ----------------------------------------------------- ticket helpers
@@ -301,7 +483,8 @@ __device__ __forceinline__ double block_reduce_max(double v, double *sh) {
 // =========================================================================
 template <int COST, int DP>
 __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
-    __shared__ Stage<COST, DP> sg;
+    __shared__ Buf<COST, DP> bufs[kNBuf<COST>];
+    __shared__ TcFor<COST> tcs_storage[1];
     __shared__ double thi[64], tlo[64];
     __shared__ double red[kPT / 32];
     __shared__ bool flag;
@@ -313,6 +496,8 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
     const bool valid = i < P.M;
     const long long jb = P.N * sp / P.S, je = P.N * (sp + 1) / P.S;
     load_exp_table(A.tab, thi, tlo);
+    TcFor<COST> &tcs = tcs_storage[0];
+    if constexpr (COST == PC_SQTC) tc_setup(tcs, P, i0);
     RowPt<COST, DP> rp;
     rp.load(P, i, valid);
     const double w = A.w, inv_eta = A.inv_eta;
@@ -325,31 +510,31 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
             mx = fma(-w, D, pot_q(P.gc[js], P.psic[js], inv_eta));
         }
     }
-    for (long long j0 = jb; j0 < je; j0 += kCC) {
-        const int nc = (int)min((long long)kCC, je - j0);
-        __syncthreads();
-        for (int c = tid; c < kCC; c += kPT) sg.q[c] = (c < nc) ? pot_q(P.gc[j0 + c], P.psic[j0 + c], inv_eta) : -INFINITY;
-        stage_cost<COST, DP>(sg, P, i0, j0, nc);
-        __syncthreads();
-        if (valid) {
+    stream_columns<COST, DP>(P, i0, jb, je, inv_eta, 0, false, bufs, &tcs,
+                             [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
+        if (!valid) return;
 #pragma unroll 4
-            for (int c = 0; c < kCC; ++c) {
-                if (c < nc) {
-                    const double D = chunk_dist<COST, DP>(sg, P, rp, i, j0 + c, c, valid);
-                    const double x = fma(-w, D, sg.q[c]);
-                    if (x > mx - kLseCut) {
-                        if (x > mx) {
-                            sm = fma(sm, pexp(mx - x, thi, tlo), 1.0);
-                            mx = x;
-                            jm = (int)(j0 + c);
-                        } else {
-                            sm += pexp(x - mx, thi, tlo);
-                        }
+        for (int c = 0; c < kCC; ++c) {
+            if (c < nc) {
+                double D;
+                if constexpr (COST == PC_SQTC) D = (double)fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
+                else if constexpr (COST == PC_DENSE_ROW) D = B.tile[c * (kPT + 1) + threadIdx.x];
+                else if constexpr (COST == PC_DENSE_COL) D = __ldg(P.C + (j0 + c) * P.ldc + i);
+                else D = rp.dist(B, c);
+                const double x = fma(-w, D, B.q[c]);
+                if (x > mx - kLseCut) {
+                    if (x > mx) {
+                        sm = fma(sm, pexp(mx - x, thi, tlo), 1.0);
+                        mx = x;
+                        jm = (int)(j0 + c);
+                    } else {
+                        sm += pexp(x - mx, thi, tlo);
                     }
                 }
             }
         }
-    }
+    });
+    if constexpr (COST == PC_SQTC) tc_teardown(tcs);
     if (valid) {
         P.pa[(long long)sp * P.M + i] = mx;
         P.pb[(long long)sp * P.M + i] = sm;
@@ -416,14 +601,16 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
 // 4 trial sum, 5 max z, 6 max count, 7 nnz side 0, 8 <a,f>+<b,g>,
 // 9 max row sum, 10 max column sum, 11 nnz side 1.
 // =========================================================================
-template <int COST, int DP>
-__device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, int bid, Stage<COST, DP> &sg,
-                                         double *thi, double *tlo, double *red, bool *flag, int side) {
+template <int COST, int DP, class TS>
+__device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, int bid, Buf<COST, DP> *bufs,
+                                         TS &tcs, double *thi, double *tlo, double *red, bool *flag,
+                                         int side) {
     const int tid = threadIdx.x;
     const int rb = bid % P.RB, sp = bid / P.RB;
     const long long i0 = (long long)rb * kPT, i = i0 + tid;
     const bool valid = i < P.M;
     const long long jb = P.N * sp / P.S, je = P.N * (sp + 1) / P.S;
+    if constexpr (COST == PC_SQTC) tc_setup(tcs, P, i0);
     RowPt<COST, DP> rp;
     rp.load(P, i, valid);
     const double w = A.w, inv_eta = A.inv_eta;
@@ -433,52 +620,46 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
         if (P.eu) { eu = P.eu[i]; bu = P.bu[i]; }
     }
     const bool trial = P.eu != nullptr, sparse = P.tau > 0.0;
+    // skip test in the form fma(-w, D, qt_j) > thr_i (qt = q + bump_j): the exact z is
+    // only formed for entries that pass (R10); near the cut the two orientations may
+    // decide differently, which changes sums by < e^-80 and never the kept pattern
+    const double thr = -kSumCut - Pi - bu;
     double acc = 0.0, cx = 0.0, em = 0.0, mz = -INFINITY;
     int cnt = 0;
     const long long bufbase = (i * P.S + sp) * P.cap;
-    for (long long j0 = jb; j0 < je; j0 += kCC) {
-        const int nc = (int)min((long long)kCC, je - j0);
-        __syncthreads();
-        for (int c = tid; c < kCC; c += kPT) {
-            double q = -INFINITY;
-            if (c < nc) q = P.m1_row ? pot_q(P.gc[j0 + c], P.psic[j0 + c], inv_eta)
-                                     : pot_p(P.gc[j0 + c], P.psic[j0 + c], inv_eta);
-            sg.q[c] = q;
-            if (trial) {
-                sg.ev[c] = (c < nc) ? P.ev[j0 + c] : 0.0;
-                sg.bv[c] = (c < nc) ? P.bv[j0 + c] : 0.0;
-            }
-        }
-        stage_cost<COST, DP>(sg, P, i0, j0, nc);
-        __syncthreads();
-        if (valid) {
+    stream_columns<COST, DP>(P, i0, jb, je, inv_eta, P.m1_row ? 0 : 1, trial, bufs, &tcs,
+                             [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
+        if (!valid) return;
 #pragma unroll 4
-            for (int c = 0; c < kCC; ++c) {
-                if (c < nc) {
-                    const double D = chunk_dist<COST, DP>(sg, P, rp, i, j0 + c, c, valid);
-                    const double z = fma(-w, D, __dadd_rn(Pi, sg.q[c]));
-                    const double zt = trial ? z + bu + sg.bv[c] : z;
-                    if (zt > -kSumCut) {
-                        const double X = pexp(z, thi, tlo);
-                        acc += X;
-                        mz = fmax(mz, z);
-                        if (P.want_cx) cx = fma(X, D, cx);
-                        if (trial) {
-                            const double ev = sg.ev[c];
-                            em = fma(X, fma(eu, ev, eu + ev), em);
+        for (int c = 0; c < kCC; ++c) {
+            if (c < nc) {
+                double D;
+                if constexpr (COST == PC_SQTC) D = (double)fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
+                else if constexpr (COST == PC_DENSE_ROW) D = B.tile[c * (kPT + 1) + threadIdx.x];
+                else if constexpr (COST == PC_DENSE_COL) D = __ldg(P.C + (j0 + c) * P.ldc + i);
+                else D = rp.dist(B, c);
+                if (fma(-w, D, B.qt[c]) > thr) {
+                    const double z = fma(-w, D, __dadd_rn(Pi, B.q[c]));
+                    const double X = pexp(z, thi, tlo);
+                    acc += X;
+                    mz = fmax(mz, z);
+                    if (P.want_cx) cx = fma(X, D, cx);
+                    if (trial) {
+                        const double ev = B.ev[c];
+                        em = fma(X, fma(eu, ev, eu + ev), em);
+                    }
+                    if (sparse && X >= P.tau) {
+                        if (cnt < P.cap) {
+                            P.bcol[bufbase + cnt] = (int)(j0 + c);
+                            P.bval[bufbase + cnt] = X;
                         }
-                        if (sparse && X >= P.tau) {
-                            if (cnt < P.cap) {
-                                P.bcol[bufbase + cnt] = (int)(j0 + c);
-                                P.bval[bufbase + cnt] = X;
-                            }
-                            ++cnt;
-                        }
+                        ++cnt;
                     }
                 }
             }
         }
-    }
+    });
+    if constexpr (COST == PC_SQTC) tc_teardown(tcs);
     if (valid) {
         P.pa[(long long)sp * P.M + i] = acc;
         if (sparse) P.cnt[i * P.S + sp] = cnt;
@@ -539,8 +720,9 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
 
 template <int COST0, int COST1, int DP>
 __global__ void __launch_bounds__(kPT) sum_pass_kernel(PassArgs A) {
-    constexpr size_t kB0 = sizeof(Stage<COST0, DP>), kB1 = sizeof(Stage<COST1, DP>);
-    __shared__ __align__(16) unsigned char smraw[kB0 > kB1 ? kB0 : kB1];
+    constexpr size_t kB0 = sizeof(Buf<COST0, DP>) * kNBuf<COST0>, kB1 = sizeof(Buf<COST1, DP>) * kNBuf<COST1>;
+    __shared__ __align__(128) unsigned char smraw[kB0 > kB1 ? kB0 : kB1];
+    __shared__ TcFor<(COST0 == PC_SQTC || COST1 == PC_SQTC) ? PC_SQTC : COST0> tcs;
     __shared__ double thi[64], tlo[64];
     __shared__ double red[kPT / 32];
     __shared__ bool flag;
@@ -548,9 +730,9 @@ __global__ void __launch_bounds__(kPT) sum_pass_kernel(PassArgs A) {
     const int side = (blockIdx.x < (unsigned)A.G0) ? 0 : 1;
     const int bid = side == 0 ? blockIdx.x : blockIdx.x - A.G0;
     if (side == 0)
-        sum_side<COST0, DP>(A, A.side[0], bid, *reinterpret_cast<Stage<COST0, DP> *>(smraw), thi, tlo, red, &flag, 0);
+        sum_side<COST0, DP>(A, A.side[0], bid, reinterpret_cast<Buf<COST0, DP> *>(smraw), tcs, thi, tlo, red, &flag, 0);
     else
-        sum_side<COST1, DP>(A, A.side[1], bid, *reinterpret_cast<Stage<COST1, DP> *>(smraw), thi, tlo, red, &flag, 1);
+        sum_side<COST1, DP>(A, A.side[1], bid, reinterpret_cast<Buf<COST1, DP> *>(smraw), tcs, thi, tlo, red, &flag, 1);
     // only row-block finalizers continue past here with flag set
     if (!flag) return;
     const unsigned tot = (unsigned)(A.side[0].RB + (A.nsides > 1 ? A.side[1].RB : 0));
@@ -691,6 +873,16 @@ __global__ void __launch_bounds__(kPT) csr_build_kernel(PassSide P0, PassSide P1
             dst += len;
         }
         if (i == P.M - 1) O.ptr[P.M] = dst;
+    }
+}
+
+// fp16 copy of padded fp32 points (rows of 16; exact for integers |x| <= 2048)
+__global__ void to_half16_kernel(long long np, int dp, const float *x32, __half *xh) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < np * 16;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long p = t >> 4;
+        const int k = (int)(t & 15);
+        xh[t] = __float2half_rn(k < dp ? x32[p * dp + k] : 0.f);
     }
 }
 

@@ -319,3 +319,34 @@ def test_edge_cases(P):
     bad = P.DeviceProblem(2, 2, 0, T(np.ones(2) / 2), T(np.ones(2) / 2), -1.0, C=T(np.zeros((2, 2))))
     with pytest.raises(RuntimeError):
         P.solve(bad)
+
+
+@pytest.mark.parametrize("name,mk", [("c3s", lambda: make("c3_gmm10k", scale=0.05)),
+                                     ("c2s", lambda: make("c2_img4k", scale=0.1)),
+                                     ("rag_sq", lambda: ragged(301, 517, 9, "sq", 10))])
+def test_tensor_core_cross_term_bit_identical(P, name, mk, monkeypatch):
+    # x.y on tcgen05 (fp16 operands, fp32 accumulate) is exact for integer points with
+    # |x| <= 2048 and partial sums < 2^24 (pins_tc.cuh), so every pass must reproduce the
+    # SIMT fp32 path bit for bit: sums, objective, CSR pattern and values, sweeps
+    w = mk()
+    C, Ck, phi, psi, s, f, g = oracle_state(w, 1)
+    tau = 1e-4 / (w.m * w.n)
+    out = []
+    for no_tc in (False, True):
+        if no_tc:
+            monkeypatch.setenv("PINS_NO_TC", "1")
+        pb = P.DeviceProblem.from_workload(w)
+        ws = P.Workspace()
+        ev = P.evaluate(ws, pb, T(phi), T(psi), s, T(f), T(g), tau=tau)
+        csr = [H(t) for t in P.get_csr(ws)]
+        fd, gd = T(f), T(g)
+        for _ in range(2):
+            P.sinkhorn_sweep(ws, pb, T(phi), T(psi), s, fd, gd)
+        out.append((H(ev["r"]), H(ev["c"]), ev["cost"], ev["grad_l1"], csr, H(fd), H(gd)))
+    a, b = out
+    for x, y in zip(a[:2], b[:2]):
+        assert np.array_equal(x, y)
+    assert a[2] == b[2] and a[3] == b[3]
+    for x, y in zip(a[4], b[4]):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a[5], b[5]) and np.array_equal(a[6], b[6])
