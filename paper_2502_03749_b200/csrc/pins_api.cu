@@ -498,8 +498,8 @@ int prepare_pass(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
     for (int q = 0; q < 2; ++q) {
         const long long M = q == 0 ? m : n, N = q == 0 ? n : m;
         const int RB = (int)((M + kPT - 1) / kPT);
-        // column splits: ~4 CTAs of 128 threads per SM per side, splits >= kCC columns
-        long long S = (4LL * ws->nsm + RB - 1) / RB;
+        // column splits: ~8 CTAs of 128 threads per SM per side, splits >= kCC columns
+        long long S = (8LL * ws->nsm + RB - 1) / RB;
         S = std::max(1LL, std::min(S, std::max(1LL, N / kCC)));
         ws->S[q] = (int)S;
         SideBufs &B = ws->sb[q];

@@ -51,6 +51,34 @@ __device__ __forceinline__ double pexp(double z, const double *__restrict__ thi,
     return res * __hiloint2double((e + 1623) << 20, 0) * 0x1p-600;
 }
 
+// exp(z) for z in [-745, 709] without range branches (callers clamp): the same
+// table and polynomial as pexp, so results agree with pexp bit for bit there.
+__device__ __forceinline__ double pexp_lean(double z, const double *__restrict__ thi,
+                                            const double *__restrict__ tlo) {
+    const double kL2E64 = 92.332482616893657;
+    const double kLn2Hi = 6.93147180369123816490e-01 * 0.015625;
+    const double kLn2Lo = 1.90821492927058770002e-10 * 0.015625;
+    const double kShift = 6755399441055744.0;
+    double t = fma(z, kL2E64, kShift);
+    double kd = t - kShift;
+    int k = __double2loint(t);
+    double r = fma(-kd, kLn2Hi, z);
+    r = fma(-kd, kLn2Lo, r);
+    double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = p * r;
+    int j = k & 63;
+    int e = k >> 6;
+    double th = thi[j];
+    double res = th + fma(th, p, tlo[j]);
+    // 2^e in two factors (e in [-1075, 1023]): exact, no denormal branch
+    const int e1 = e >> 1, e2 = e - e1;
+    return res * __hiloint2double((e1 + 1023) << 20, 0) * __hiloint2double((e2 + 1023) << 20, 0);
+}
+
 __device__ __forceinline__ void load_exp_table(const ExpTable *__restrict__ g, double *shi,
                                                double *slo) {
     for (int t = threadIdx.x; t < 64; t += blockDim.x) {

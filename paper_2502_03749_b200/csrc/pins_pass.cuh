@@ -440,6 +440,16 @@ __device__ __forceinline__ void tc_teardown(TS &T) {
     }
 }
 
+// D(i, j0 + c) for the non-tensor-core costs from the staged chunk
+template <int COST, int DP>
+__device__ __forceinline__ double chunk_dist(const Buf<COST, DP> &B, const PassSide &P, const RowPt<COST, DP> &rp,
+                                             long long i, long long j0, int c) {
+    if constexpr (COST == PC_DENSE_ROW) return B.tile[c * (kPT + 1) + threadIdx.x];
+    else if constexpr (COST == PC_DENSE_COL) return __ldg(P.C + (j0 + c) * P.ldc + i);
+    else if constexpr (COST == PC_SQTC) return 0.0;
+    else return rp.dist(B, c);
+}
+
 // ----------------------------------------------------- ticket helpers
 // returns true in exactly one CTA: the last of `total` arrivals on *t (then reset)
 __device__ __forceinline__ bool last_arrival(unsigned *t, unsigned total, bool *sh_flag) {
@@ -485,6 +495,7 @@ template <int COST, int DP>
 __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
     __shared__ Buf<COST, DP> bufs[kNBuf<COST>];
     __shared__ TcFor<COST> tcs_storage[1];
+    __shared__ float dscr[COST == PC_SQTC ? kPT * (kCC + 1) : 1];
     __shared__ double thi[64], tlo[64];
     __shared__ double red[kPT / 32];
     __shared__ bool flag;
@@ -510,28 +521,40 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
             mx = fma(-w, D, pot_q(P.gc[js], P.psic[js], inv_eta));
         }
     }
+    float *dsc = dscr + tid * (kCC + 1);       // PC_SQTC: this thread's chunk distances
     stream_columns<COST, DP>(P, i0, jb, je, inv_eta, 0, false, bufs, &tcs,
                              [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
         if (!valid) return;
-#pragma unroll 4
+        // phase 1 (branch-free): skip test against the chunk-start bound of the row max
+        const double thr = mx - kLseCut;
+        unsigned mask = 0u;
+#pragma unroll
         for (int c = 0; c < kCC; ++c) {
-            if (c < nc) {
-                double D;
-                if constexpr (COST == PC_SQTC) D = (double)fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
-                else if constexpr (COST == PC_DENSE_ROW) D = B.tile[c * (kPT + 1) + threadIdx.x];
-                else if constexpr (COST == PC_DENSE_COL) D = __ldg(P.C + (j0 + c) * P.ldc + i);
-                else D = rp.dist(B, c);
-                const double x = fma(-w, D, B.q[c]);
-                if (x > mx - kLseCut) {
-                    if (x > mx) {
-                        sm = fma(sm, pexp(mx - x, thi, tlo), 1.0);
-                        mx = x;
-                        jm = (int)(j0 + c);
-                    } else {
-                        sm += pexp(x - mx, thi, tlo);
-                    }
-                }
+            double D;
+            if constexpr (COST == PC_SQTC) {
+                const float Df = fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
+                dsc[c] = Df;
+                D = (double)Df;
+            } else {
+                D = chunk_dist<COST, DP>(B, P, rp, i, j0, c);
             }
+            const double x = fma(-w, D, B.q[c]);
+            mask |= (c < nc && x > thr) ? (1u << c) : 0u;
+        }
+        // phase 2: the surviving entries of this row, in column order (one exp each)
+        while (mask) {
+            const int c = __ffs(mask) - 1;
+            mask &= mask - 1u;
+            double D;
+            if constexpr (COST == PC_SQTC) D = (double)dsc[c];
+            else D = chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+            const double x = fma(-w, D, B.q[c]);
+            const double d = x - mx;
+            const double e = pexp_lean(fmax(-745.0, -fabs(d)), thi, tlo);
+            const bool up = d > 0.0;
+            sm = up ? fma(sm, e, 1.0) : sm + e;
+            mx = up ? x : mx;
+            jm = up ? (int)(j0 + c) : jm;
         }
     });
     if constexpr (COST == PC_SQTC) tc_teardown(tcs);
@@ -603,8 +626,8 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
 // =========================================================================
 template <int COST, int DP, class TS>
 __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, int bid, Buf<COST, DP> *bufs,
-                                         TS &tcs, double *thi, double *tlo, double *red, bool *flag,
-                                         int side) {
+                                         TS &tcs, float *dscr, double *thi, double *tlo, double *red,
+                                         bool *flag, int side) {
     const int tid = threadIdx.x;
     const int rb = bid % P.RB, sp = bid / P.RB;
     const long long i0 = (long long)rb * kPT, i = i0 + tid;
@@ -627,35 +650,44 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
     double acc = 0.0, cx = 0.0, em = 0.0, mz = -INFINITY;
     int cnt = 0;
     const long long bufbase = (i * P.S + sp) * P.cap;
+    float *dsc = dscr + tid * (kCC + 1);
     stream_columns<COST, DP>(P, i0, jb, je, inv_eta, P.m1_row ? 0 : 1, trial, bufs, &tcs,
                              [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
         if (!valid) return;
-#pragma unroll 4
+        unsigned mask = 0u;
+#pragma unroll
         for (int c = 0; c < kCC; ++c) {
-            if (c < nc) {
-                double D;
-                if constexpr (COST == PC_SQTC) D = (double)fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
-                else if constexpr (COST == PC_DENSE_ROW) D = B.tile[c * (kPT + 1) + threadIdx.x];
-                else if constexpr (COST == PC_DENSE_COL) D = __ldg(P.C + (j0 + c) * P.ldc + i);
-                else D = rp.dist(B, c);
-                if (fma(-w, D, B.qt[c]) > thr) {
-                    const double z = fma(-w, D, __dadd_rn(Pi, B.q[c]));
-                    const double X = pexp(z, thi, tlo);
-                    acc += X;
-                    mz = fmax(mz, z);
-                    if (P.want_cx) cx = fma(X, D, cx);
-                    if (trial) {
-                        const double ev = B.ev[c];
-                        em = fma(X, fma(eu, ev, eu + ev), em);
-                    }
-                    if (sparse && X >= P.tau) {
-                        if (cnt < P.cap) {
-                            P.bcol[bufbase + cnt] = (int)(j0 + c);
-                            P.bval[bufbase + cnt] = X;
-                        }
-                        ++cnt;
-                    }
+            double D;
+            if constexpr (COST == PC_SQTC) {
+                const float Df = fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
+                dsc[c] = Df;
+                D = (double)Df;
+            } else {
+                D = chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+            }
+            mask |= (c < nc && fma(-w, D, B.qt[c]) > thr) ? (1u << c) : 0u;
+        }
+        while (mask) {
+            const int c = __ffs(mask) - 1;
+            mask &= mask - 1u;
+            double D;
+            if constexpr (COST == PC_SQTC) D = (double)dsc[c];
+            else D = chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+            const double z = fma(-w, D, __dadd_rn(Pi, B.q[c]));
+            const double X = pexp_lean(fmin(709.0, fmax(-745.0, z)), thi, tlo);
+            acc += X;
+            mz = fmax(mz, z);
+            if (P.want_cx) cx = fma(X, D, cx);
+            if (trial) {
+                const double ev = B.ev[c];
+                em = fma(X, fma(eu, ev, eu + ev), em);
+            }
+            if (sparse && X >= P.tau) {
+                if (cnt < P.cap) {
+                    P.bcol[bufbase + cnt] = (int)(j0 + c);
+                    P.bval[bufbase + cnt] = X;
                 }
+                ++cnt;
             }
         }
     });
@@ -723,6 +755,7 @@ __global__ void __launch_bounds__(kPT) sum_pass_kernel(PassArgs A) {
     constexpr size_t kB0 = sizeof(Buf<COST0, DP>) * kNBuf<COST0>, kB1 = sizeof(Buf<COST1, DP>) * kNBuf<COST1>;
     __shared__ __align__(128) unsigned char smraw[kB0 > kB1 ? kB0 : kB1];
     __shared__ TcFor<(COST0 == PC_SQTC || COST1 == PC_SQTC) ? PC_SQTC : COST0> tcs;
+    __shared__ float dscr[(COST0 == PC_SQTC || COST1 == PC_SQTC) ? kPT * (kCC + 1) : 1];
     __shared__ double thi[64], tlo[64];
     __shared__ double red[kPT / 32];
     __shared__ bool flag;
@@ -730,9 +763,9 @@ __global__ void __launch_bounds__(kPT) sum_pass_kernel(PassArgs A) {
     const int side = (blockIdx.x < (unsigned)A.G0) ? 0 : 1;
     const int bid = side == 0 ? blockIdx.x : blockIdx.x - A.G0;
     if (side == 0)
-        sum_side<COST0, DP>(A, A.side[0], bid, reinterpret_cast<Buf<COST0, DP> *>(smraw), tcs, thi, tlo, red, &flag, 0);
+        sum_side<COST0, DP>(A, A.side[0], bid, reinterpret_cast<Buf<COST0, DP> *>(smraw), tcs, dscr, thi, tlo, red, &flag, 0);
     else
-        sum_side<COST1, DP>(A, A.side[1], bid, reinterpret_cast<Buf<COST1, DP> *>(smraw), tcs, thi, tlo, red, &flag, 1);
+        sum_side<COST1, DP>(A, A.side[1], bid, reinterpret_cast<Buf<COST1, DP> *>(smraw), tcs, dscr, thi, tlo, red, &flag, 1);
     // only row-block finalizers continue past here with flag set
     if (!flag) return;
     const unsigned tot = (unsigned)(A.side[0].RB + (A.nsides > 1 ? A.side[1].RB : 0));
