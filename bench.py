@@ -110,7 +110,8 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ work model
-def kernel_roofline(cls: str, w, launches: int, ms: float, clocks_mhz: float, peaks: dict, counts: dict) -> dict:
+def kernel_roofline(cls: str, w, launches: int, ms: float, clocks_mhz: float, peaks: dict, counts: dict,
+                    work: float = 0.0) -> dict:
     """Roofline entry for one kernel class (DESIGN.md §7 gives every number used here).
 
     sweep_row / eval (dense passes over the m x n block):
@@ -140,13 +141,13 @@ def kernel_roofline(cls: str, w, launches: int, ms: float, clocks_mhz: float, pe
                 "frac": ach / peak, "work_per_launch": f"{entries:.3g} entries",
                 "peak_source": f"derived: 148 SM x 4 issue x 32 lanes x {clocks_mhz:.0f} MHz / (d+3={d + 3}) instr per entry"}
     if cls == "cg":
-        its = counts.get("cg_iters", 0) / max(1, counts.get("newton_iters", 1))
-        nnz = counts.get("nnz_late", 2 * (w.m + w.n))
-        byts = its * (24.0 * nnz + 64.0 * (w.m + w.n))
+        # bytes counted by the library per launch from each CG's own iteration count
+        # and nnz (pins_prof_read_work): 24 B x nnz + 80 B x (m + n) per iteration
+        byts = work / max(1, launches)
         ach = byts / avg_s / 1e9
         peak = peaks.get("hbm_gbs", 6650.0)
         return {"kernel": cls, "bound": "hbm", "unit": "GB/s", "achieved": ach, "peak": peak, "frac": ach / peak,
-                "work_per_launch": f"{byts:.3g} B ({its:.0f} it x (24 B x nnz {nnz} + 64 B x (m+n)))",
+                "work_per_launch": f"{byts:.3g} B (library-counted: 24 B x nnz + 80 B x (m+n) per CG iteration)",
                 "peak_source": "measured" if "hbm_gbs" in peaks else "fallback"}
     return {"kernel": cls}
 
@@ -342,7 +343,7 @@ def main():
         kerns = {}
         for c in ("sweep_row", "eval", "cg"):
             if prof[c]["launches"]:
-                e = kernel_roofline(c, w, prof[c]["launches"], prof[c]["ms"], mhz, peaks, counts)
+                e = kernel_roofline(c, w, prof[c]["launches"], prof[c]["ms"], mhz, peaks, counts, prof[c]["work"])
                 e.update(launches=prof[c]["launches"], avg_launch_us=prof[c]["ms"] / prof[c]["launches"] * 1e3,
                          share_of_device_time=prof[c]["ms"] / max(total_ms, 1e-9), traffic=None)
                 kerns[c] = e

@@ -15,6 +15,7 @@
 #include "pins_pass.cuh"
 #include "pins_cg.cuh"
 #include "pins_order.cuh"
+#include "pins_tree.cuh"
 
 using namespace pins;
 
@@ -53,6 +54,7 @@ struct Prof {
     bool on = false;
     long long launches[PINS_PROF_NCLASS] = {};
     double ms[PINS_PROF_NCLASS] = {};
+    double work[PINS_PROF_NCLASS] = {};   // algorithmic bytes / entries, where the host knows them
     std::vector<cudaEvent_t> pool;
     struct Pend { int cls; cudaEvent_t a, b; };
     std::vector<Pend> pend;
@@ -100,7 +102,12 @@ struct ProfScope {
 extern "C" void pins_prof_enable(int32_t on) { g_prof.on = on != 0; }
 extern "C" void pins_prof_reset(void) {
     g_prof.fold();
-    for (int c = 0; c < PINS_PROF_NCLASS; ++c) { g_prof.launches[c] = 0; g_prof.ms[c] = 0.0; }
+    for (int c = 0; c < PINS_PROF_NCLASS; ++c) { g_prof.launches[c] = 0; g_prof.ms[c] = 0.0; g_prof.work[c] = 0.0; }
+}
+extern "C" int pins_prof_read_work(int32_t cls, double *work) {
+    PINS_ARG(cls >= 0 && cls < PINS_PROF_NCLASS && work, "class / pointer");
+    *work = g_prof.work[cls];
+    return PINS_OK;
 }
 extern "C" int pins_prof_read(int32_t cls, int64_t *launches, double *ms) {
     PINS_ARG(cls >= 0 && cls < PINS_PROF_NCLASS && launches && ms, "class / pointers");
@@ -145,6 +152,7 @@ struct pins_workspace {
     DevBuf colpart, blk, rowsum, gradf, colsum, gradg, rowcnt, rb_col, rb_val;
     DevBuf rowptr, colidx, val, colcnt, colptr, cursor, rowidx, valT;
     DevBuf cgvec, cgpart, cgst, st, ft, gt, eu, ev, bu, bv, dir, rhs, tab, fsave, gsave, uv;
+    DevBuf tr_i, tr_d, tr_u8, tr_u64;   // tree-CG workspace (int / double / byte / u64 pools)
     // v2 dense passes
     SideBufs sb[2];
     DevBuf x32, y32, x64, y64, nx32, ny32, xh, yh, pinfo, ctl, gticket, pst, tol;
@@ -156,6 +164,9 @@ struct pins_workspace {
     long long pcap = 16;       // per (row, split) sparsify capacity
     long long m = 0, n = 0, cap = 64, nnz = 0;
     int G = 0, nsm = 0, dev = -1;
+    bool tree_valid = false;
+    long long tree_N = -1;
+    int tree_last_its = 0, tree_backoff = 0;
     bool csr_ready = false, csc_ready = false;
     double *h = nullptr;   // pinned host scalars (64)
 };
@@ -206,7 +217,8 @@ extern "C" void pins_workspace_destroy(pins_workspace *ws) {
                       &ws->cgpart, &ws->cgst, &ws->st, &ws->ft, &ws->gt, &ws->eu, &ws->ev,
                       &ws->dir, &ws->rhs, &ws->tab, &ws->fsave, &ws->gsave, &ws->uv, &ws->bu, &ws->bv,
                       &ws->x32, &ws->y32, &ws->x64, &ws->y64, &ws->nx32, &ws->ny32, &ws->xh, &ws->yh, &ws->pinfo,
-                      &ws->ctl, &ws->gticket, &ws->pst, &ws->tol};
+                      &ws->ctl, &ws->gticket, &ws->pst, &ws->tol,
+                      &ws->tr_i, &ws->tr_d, &ws->tr_u8, &ws->tr_u64};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     for (int q = 0; q < 2; ++q) {
@@ -962,6 +974,122 @@ int run_cg_cluster(pins_workspace *ws, long long m, long long n, double mu, cons
     return PINS_OK;
 }
 
+
+// ---- spanning-tree preconditioned CG, one CTA (pins_tree.cuh) ----
+constexpr int kTreeMaxNodes = 26000;               // tree-solve vector in shared memory
+constexpr long long kTreeNnzMax = 400000;
+bool use_tree_cg(pins_workspace *ws, long long m, long long n) {
+    const char *e = getenv("PINS_CG");
+    if (e && strcmp(e, "tree") != 0) return false;
+    // near-tree supports only (late EPPA: nnz ~ m + n, Thm 4.3); with many
+    // off-tree edges the tree preconditioner loses its edge over Jacobi
+    // adaptive: after a tree solve that needed many iterations (support far from
+    // a tree), use the Jacobi-Schur cluster CG for a while, then try again
+    const bool forced = e && strcmp(e, "tree") == 0;
+    if (!forced && ws->tree_backoff > 0) {
+        --ws->tree_backoff;
+        return false;
+    }
+    // the tree preconditioner pays off when the support is close to a spanning tree
+    // (late EPPA iterations); far from it the Jacobi-Schur cluster CG is faster
+    const bool near_tree = (double)ws->nnz <= 1.25 * (double)(m + n);
+    return (forced || near_tree) && m + n <= kTreeMaxNodes && ws->nnz <= kTreeNnzMax && ws->csc_ready;
+}
+
+int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const double *rhs, double *x,
+                double rtol, int maxit, const double *gradf, const double *gradg, const double *a,
+                const double *b, cudaStream_t st) {
+    const long long N = m + n, nnz = std::max<long long>(ws->nnz, 1);
+    PINS_TRY(ensure(ws->cgst, sizeof(double) * 16));
+    // persistent arrays first, nnz-sized scratch last (offsets stay put as nnz changes)
+    // comp hook tptr tnbr(2) deg fu fv1 fv2 tei tej tsrc(2) fs1 fs2 = 15 N, + rstart, ctr
+    const long long ni_fixed = 15 * N + 1 + kTreeMaxRounds + 1 + 8;
+    const long long ni = ni_fixed + nnz;
+    const long long nd = 2 * N + N + 3 * N + 4 * N + 3 * N;   // tw, dcur, fc1/fc2/finv, r z p q, tval fw1 fw2
+    const void *old_i = ws->tr_i.p, *old_d = ws->tr_d.p;
+    PINS_TRY(ensure(ws->tr_i, sizeof(int) * ni));
+    PINS_TRY(ensure(ws->tr_d, sizeof(double) * nd));
+    PINS_TRY(ensure(ws->tr_u8, (size_t)(nnz + 2 * N)));
+    PINS_TRY(ensure(ws->tr_u64, sizeof(unsigned long long) * N));
+    if (ws->tr_i.p != old_i || ws->tr_d.p != old_d || ws->tree_N != N) ws->tree_valid = false;
+    TreeArgs A;
+    memset(&A, 0, sizeof A);
+    A.m = (int)m;
+    A.n = (int)n;
+    A.nnz = ws->nnz;
+    A.rowptr = ptr<long long>(ws->rowptr);
+    A.colidx = ptr<int>(ws->colidx);
+    A.val = ptr<double>(ws->val);
+    A.colptr = ptr<long long>(ws->colptr);
+    A.rowidx = ptr<int>(ws->rowidx);
+    A.valT = ptr<double>(ws->valT);
+    A.dr = ptr<double>(ws->rowsum);
+    A.dc = ptr<double>(ws->colsum);
+    A.mu = mu;
+    A.rhs = rhs;
+    A.x = x;
+    A.rtol = rtol;
+    A.maxit = maxit;
+    A.gradf = gradf;
+    A.gradg = gradg;
+    A.a = a;
+    A.b = b;
+    A.st = ptr<double>(ws->cgst);
+    int *ip = ptr<int>(ws->tr_i);
+    A.comp = ip; ip += N;
+    A.hook = ip; ip += N;
+    A.tptr = ip; ip += N + 1;
+    A.tnbr = ip; ip += 2 * N;
+    A.deg = ip; ip += N;
+    A.fu = ip; ip += N;
+    A.fv1 = ip; ip += N;
+    A.fv2 = ip; ip += N;
+    A.rstart = ip; ip += kTreeMaxRounds + 1;
+    A.ctr = ip; ip += 8;
+    A.tei = ip; ip += N;
+    A.tej = ip; ip += N;
+    A.tsrc = ip; ip += 2 * N;
+    A.fs1 = ip; ip += N;
+    A.fs2 = ip; ip += N;
+    A.erow = ip;
+    double *dp_ = ptr<double>(ws->tr_d);
+    A.tw = dp_; dp_ += 2 * N;
+    A.dcur = dp_; dp_ += N;
+    A.fc1 = dp_; dp_ += N;
+    A.fc2 = dp_; dp_ += N;
+    A.finv = dp_; dp_ += N;
+    A.r = dp_; dp_ += N;
+    A.z = dp_; dp_ += N;
+    A.p = dp_; dp_ += N;
+    A.q = dp_; dp_ += N;
+    A.tval = dp_; dp_ += N;
+    A.fw1 = dp_; dp_ += N;
+    A.fw2 = dp_;
+    unsigned char *bp = ptr<unsigned char>(ws->tr_u8);
+    A.alive = bp; bp += N;
+    A.sel = bp; bp += N;
+    A.tmark = bp;
+    A.best = ptr<unsigned long long>(ws->tr_u64);
+    // reuse the stored tree while it keeps CG short (the kernel also checks that
+    // every tree edge is still in the support and rebuilds otherwise)
+    A.reuse = ws->tree_valid && ws->tree_last_its <= 48 ? 1 : 0;
+    const size_t base = sizeof(double) * (size_t)N;
+    const size_t budget = 220 * 1024;
+    A.tail_cap = base < budget ? (int)((budget - base) / 40) : 0;
+    const size_t smem = base + (size_t)A.tail_cap * 40;
+    static size_t configured = 0;
+    if (smem > configured) {
+        PINS_CUDA(cudaFuncSetAttribute(tree_pcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<size_t>(smem, 48 * 1024)));
+        configured = std::max<size_t>(smem, 48 * 1024);
+    }
+    LAUNCH(PINS_PROF_CG, st, tree_pcg_kernel<<<1, kTT, smem, st>>>(A));
+    PINS_CUDA(cudaGetLastError());
+    ws->tree_valid = true;
+    ws->tree_N = N;
+    return PINS_OK;
+}
+
 double cg_rtol(const pins_params *p, double gnorm) {
     if (p->cg_forcing <= 0.0 || gnorm <= 0.0) return p->cg_tol;
     return std::min(0.5, std::max(p->cg_tol, p->cg_forcing * p->newton_tol / gnorm));
@@ -990,7 +1118,11 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
     const double mu = prm->mu_rel * std::max(cur->maxr, cur->maxc);
     const double rtol = cg_rtol(prm, cur->gnorm);
     double *d = ptr<double>(ws->dir);
-    if (use_cluster_cg(ws, m, n)) {
+    const bool used_tree = use_tree_cg(ws, m, n);
+    if (used_tree) {
+        PINS_TRY(run_cg_tree(ws, m, n, mu, rhs, d, rtol, prm->cg_maxit, ptr<double>(ws->gradf),
+                             ptr<double>(ws->gradg), pb->a, pb->b, st));
+    } else if (use_cluster_cg(ws, m, n) && !(getenv("PINS_CG") && strcmp(getenv("PINS_CG"), "cluster") != 0)) {
         PINS_TRY(run_cg_cluster(ws, m, n, mu, rhs, d, rtol, prm->cg_maxit, ptr<double>(ws->gradf),
                                 ptr<double>(ws->gradg), pb->a, pb->b, st));
     } else {
@@ -1001,6 +1133,25 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
     PINS_CUDA(cudaMemcpyAsync(ws->h + 16, ws->cgst.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
     PINS_CUDA(cudaStreamSynchronize(st));
     const double cg_its = ws->h[16], relres = ws->h[17], slope = ws->h[18], ad = ws->h[19];
+    // algorithmic bytes of this CG launch: per iteration the CSR + CSC (12 B per
+    // entry each) and ~10 vector streams of m + n doubles
+    g_prof.work[PINS_PROF_CG] += cg_its * (24.0 * (double)ws->nnz + 80.0 * (double)N);
+    if (used_tree) {
+        ws->tree_last_its = (int)cg_its;
+        if (cg_its > 80) ws->tree_backoff = 256;
+    }
+    if (getenv("PINS_TREE_STATS") && used_tree) {    // dev instrumentation
+        double hs[16];
+        cudaMemcpy(hs, ws->cgst.p, sizeof hs, cudaMemcpyDeviceToHost);
+        static double acc[8] = {0};
+        static long calls = 0;
+        for (int q = 0; q < 7; ++q) acc[q] += hs[4 + q];
+        acc[7] += hs[11];
+        ++calls;
+        if (calls % 200 == 1)
+            fprintf(stderr, "tree-cg calls %ld nnz %lld its %.0f rebuilds %.0f | Mcycles mst %.1f fac %.1f pc %.1f mv %.1f total %.1f\n",
+                    calls, ws->nnz, cg_its, acc[7], acc[2] / 1e6, acc[3] / 1e6, acc[4] / 1e6, acc[5] / 1e6, acc[6] / 1e6);
+    }
     info[3] = cg_its;
     info[4] = relres;
     double alpha = 1.0;

@@ -1,0 +1,585 @@
+// pins_tree.cuh -- CG on the sparsified Newton system with a maximum-spanning-
+// tree preconditioner (support-graph preconditioning), one CTA per system.
+//
+// System (Alg. 2 line 12, reading R5):  M d = rhs,
+//     M = [[Dr, X],[X^T, Dc]],  Dr = diag(X~ e) + mu,  Dc = diag(X~^T e) + mu,
+// X = the sparsified plan block.  M is the "signless Laplacian" of the
+// bipartite support graph (rows + columns, edge (i, j) of weight X_ij) plus a
+// positive diagonal excess (dropped mass, mu).  The preconditioner keeps the
+// diagonal and the edges of a MAXIMUM-WEIGHT SPANNING FOREST T of that graph:
+//     M_T = diag(Dr, Dc) + T,
+// which is SPD and is factorised EXACTLY with zero fill by tree contraction.
+// Late in EPPA the plan approaches a vertex of the transport polytope, whose
+// support is a spanning tree (Thm 4.3), so M_T ~ M and CG
+// needs a handful of iterations instead of hundreds.
+//
+//  1. Boruvka: every component takes its heaviest outgoing edge (64-bit atomic
+//     max of (float weight bits, edge id): a strict total order, hence no
+//     cycles), components merge by hooking + pointer jumping; O(log N) rounds.
+//  2. Tree contraction: each round eliminates an independent set of nodes of
+//     degree <= 2 (random priorities; leaves = rake, degree 2 = compress, which
+//     rewires the two neighbours to each other with the fill weight
+//     -w1 w2 / d).  O(log N) rounds; the eliminated nodes of a round are
+//     stored contiguously with their neighbours and multipliers.
+//  3. PCG (Jacobi-free: z = M_T^-1 r): forward elimination round by round,
+//     back substitution in reverse, on a shared-memory copy of the vector.
+//
+// Everything runs in ONE CTA of kTT threads with __syncthreads between phases
+// (no grid synchronisation); graph state lives in a workspace in global
+// memory (L2-resident at these sizes), the tree-solve vector in shared memory.
+#pragma once
+#include "pins_device.cuh"
+
+namespace pins {
+
+constexpr int kTT = 1024;              // threads of the tree-CG CTA
+constexpr int kTreeMaxRounds = 256;
+
+struct TreeArgs {
+    int m, n;                          // rows / columns (N = m + n nodes)
+    long long nnz;
+    const long long *rowptr;           // CSR of X (m rows)
+    const int *colidx;
+    const double *val;
+    const long long *colptr;           // CSC of X (n columns)
+    const int *rowidx;
+    const double *valT;
+    const double *dr, *dc;             // diagonals (without mu)
+    double mu;
+    const double *rhs;                 // N
+    double *x;                         // N (output)
+    double rtol;
+    int maxit;
+    const double *gradf, *gradg, *a, *b;   // optional slope terms
+    double *st;                        // [0] its [1] relres [2] slope [3] <(a,b),d> [4] rounds [5] tree edges
+    // workspace (global)
+    int *erow;                         // [nnz] row of each CSR entry
+    int *comp, *hook;                  // [N]
+    unsigned long long *best;          // [N]
+    unsigned char *tmark;              // [nnz]
+    int *tptr;                         // [N + 1]
+    int *tnbr;                         // [2 (N - 1)] (rewired during contraction)
+    double *tw;                        // [2 (N - 1)]
+    int *deg;                          // [N]
+    unsigned char *alive, *sel;        // [N]
+    double *dcur;                      // [N]
+    int *fu, *fv1, *fv2;               // [N] factor in elimination order
+    double *fc1, *fc2, *finv;          // [N]
+    int *rstart;                       // [kTreeMaxRounds + 1]
+    double *r, *z, *p, *q;             // [N] CG vectors
+    int *ctr;                          // [8] counters: [0] records [1] rounds [2] tree edges [3] valid
+    int tail_cap;                      // factor records cached in shared memory
+    // reuse across Newton steps: tree edge list, slot sources, weights
+    int *tei, *tej;                    // [N] tree edges (row, column)
+    double *tval;                      // [N] current weights X_ij of the tree edges
+    int *tsrc;                         // [2 (N - 1)] adjacency slot source: edge t >= 0, fill -(pos+1)
+    int *fs1, *fs2;                    // [N] record slot sources
+    double *fw1, *fw2;                 // [N] record slot weights
+    int reuse;                         // 1: try the stored tree / schedule first
+};
+
+__device__ __forceinline__ unsigned hash_prio(unsigned u, unsigned r) {
+    unsigned h = u * 0x9E3779B1u ^ (r + 1u) * 0x85EBCA6Bu;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    h *= 0x297A2D39u;
+    h ^= h >> 15;
+    return h;
+}
+
+__device__ __forceinline__ double tree_block_sum(double v, double *sh) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (warp == 0) t = warp_sum(sh[lane]);
+    if (threadIdx.x == 0) sh[32] = t;
+    __syncthreads();
+    return sh[32];
+}
+
+// smem double atomic add (CAS loop; conflicts are rare: a node receives at most
+// one update per eliminated neighbour per round)
+__device__ __forceinline__ void sm_add(double *p, double v) { atomicAdd(p, v); }
+
+// block-wide exclusive scan of per-thread counts (kTT threads); returns the
+// thread's offset, *total gets the sum
+__device__ __forceinline__ int block_excl_scan(int v, int *wsc, int *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+    }
+    __syncthreads();
+    if (lane == 31) wsc[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = wsc[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += t;
+        }
+        wsc[lane] = w;
+    }
+    __syncthreads();
+    *total = wsc[31];
+    return x - v + (warp > 0 ? wsc[warp - 1] : 0);
+}
+
+__global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
+    extern __shared__ __align__(16) unsigned char dyn[];   // 8 N bytes, reused by phase
+    __shared__ double red[40];
+    __shared__ int wsc[32];
+    __shared__ int s_flag, s_cnt;
+    const int tid = threadIdx.x;
+    const int m = A.m, n = A.n, N = m + n;
+    const long long nnz = A.nnz;
+    const double mu = A.mu;
+    const long long t_start = clock64();
+    long long t_mst = 0, t_fac = 0, t_pc = 0, t_mv = 0;
+
+    int nrounds = 0;
+    // ---------------- 0. reuse: are all stored tree edges still in the support? ----------------
+    bool rebuilt = true;
+    if (A.reuse) {
+        if (tid == 0) s_flag = 1;
+        __syncthreads();
+        const int ne = A.ctr[2];
+        for (int t = tid; t < ne; t += kTT) {
+            const int i = A.tei[t], j = A.tej[t];
+            long long lo = A.rowptr[i], hi = A.rowptr[i + 1] - 1;
+            double wv = -1.0;
+            while (lo <= hi) {                     // columns ascending inside a CSR row
+                const long long mid = (lo + hi) >> 1;
+                const int cj = A.colidx[mid];
+                if (cj == j) { wv = A.val[mid]; break; }
+                if (cj < j) lo = mid + 1; else hi = mid - 1;
+            }
+            if (wv < 0.0) s_flag = 0;
+            A.tval[t] = wv;
+        }
+        __syncthreads();
+        if (s_flag) {
+            // numeric refactorisation on the stored schedule (push updates, round by round)
+            nrounds = A.ctr[1];
+            for (int v = tid; v < N; v += kTT) A.dcur[v] = (v < m ? A.dr[v] : A.dc[v - m]) + mu;
+            __syncthreads();
+            for (int rr = 0; rr < nrounds; ++rr) {
+                const int q1 = A.rstart[rr + 1];
+                for (int q = A.rstart[rr] + tid; q < q1; q += kTT) {
+                    const int s1 = A.fs1[q], s2 = A.fs2[q];
+                    double w1 = 0.0, w2 = 0.0;
+                    if (A.fv1[q] >= 0) {
+                        if (s1 >= 0) w1 = A.tval[s1];
+                        else { const int p0 = -s1 - 1; w1 = -A.fw1[p0] * A.fw2[p0] * A.finv[p0]; }
+                    }
+                    if (A.fv2[q] >= 0) {
+                        if (s2 >= 0) w2 = A.tval[s2];
+                        else { const int p0 = -s2 - 1; w2 = -A.fw1[p0] * A.fw2[p0] * A.finv[p0]; }
+                    }
+                    const double inv = 1.0 / A.dcur[A.fu[q]];
+                    A.fw1[q] = w1;
+                    A.fw2[q] = w2;
+                    A.fc1[q] = w1 * inv;
+                    A.fc2[q] = w2 * inv;
+                    A.finv[q] = inv;
+                    if (A.fv1[q] >= 0) atomicAdd(A.dcur + A.fv1[q], -w1 * w1 * inv);
+                    if (A.fv2[q] >= 0) atomicAdd(A.dcur + A.fv2[q], -w2 * w2 * inv);
+                }
+                __syncthreads();
+            }
+            rebuilt = false;
+        }
+    }
+    if (rebuilt) {
+    // ---------------- 1. maximum spanning forest (Boruvka), state in smem ----------------
+    int *comp = reinterpret_cast<int *>(dyn);                 // N
+    unsigned *bw = reinterpret_cast<unsigned *>(dyn) + N;     // N: best weight bits, then hook
+    for (int i = tid; i < m; i += kTT)
+        for (long long e = A.rowptr[i]; e < A.rowptr[i + 1]; ++e) A.erow[e] = i;
+    for (int v = tid; v < N; v += kTT) comp[v] = v;
+    for (long long e = tid; e < nnz; e += kTT) A.tmark[e] = 0;
+    __syncthreads();
+    for (int round = 0; round < 64; ++round) {
+        for (int v = tid; v < N; v += kTT) {
+            bw[v] = 0u;
+            A.hook[v] = -1;                                   // best edge id
+        }
+        if (tid == 0) s_flag = 0;
+        __syncthreads();
+        for (long long e = tid; e < nnz; e += kTT) {
+            const int cu = comp[A.erow[e]], cv = comp[m + A.colidx[e]];
+            if (cu == cv) continue;
+            const unsigned wb = __float_as_uint((float)A.val[e]);
+            atomicMax(bw + cu, wb);
+            atomicMax(bw + cv, wb);
+        }
+        __syncthreads();
+        for (long long e = tid; e < nnz; e += kTT) {          // heaviest edge, ties -> largest id
+            const int cu = comp[A.erow[e]], cv = comp[m + A.colidx[e]];
+            if (cu == cv) continue;
+            const unsigned wb = __float_as_uint((float)A.val[e]);
+            if (wb == bw[cu]) atomicMax(A.hook + cu, (int)e);
+            if (wb == bw[cv]) atomicMax(A.hook + cv, (int)e);
+        }
+        __syncthreads();
+        for (int c = tid; c < N; c += kTT) {
+            int h = c;
+            const int e = A.hook[c];
+            if (comp[c] == c && e >= 0) {
+                const int cu = comp[A.erow[e]], cv = comp[m + A.colidx[e]];
+                const int other = cu == c ? cv : cu;
+                if (!(A.hook[other] == e && c < other)) h = other;   // mutual: smaller id stays
+                A.tmark[e] = 1;
+                s_flag = 1;
+            }
+            bw[c] = (unsigned)h;                              // bw reused as the hook target
+        }
+        __syncthreads();
+        if (!s_flag) break;
+        for (int v = tid; v < N; v += kTT) comp[v] = (int)bw[comp[v]];
+        __syncthreads();
+        for (int it = 0; it < 40; ++it) {                     // pointer jumping
+            if (tid == 0) s_cnt = 0;
+            __syncthreads();
+            for (int v = tid; v < N; v += kTT) {
+                const int c = comp[v], cc = comp[c];
+                if (c != cc) { comp[v] = cc; s_cnt = 1; }
+            }
+            __syncthreads();
+            if (!s_cnt) break;
+        }
+    }
+    t_mst = clock64() - t_start;
+
+    // ---------------- 2. tree adjacency (CSR of the forest) ----------------
+    for (int v = tid; v <= N; v += kTT) A.tptr[v] = 0;
+    __syncthreads();
+    for (long long e = tid; e < nnz; e += kTT)
+        if (A.tmark[e]) {
+            atomicAdd(A.tptr + A.erow[e] + 1, 1);
+            atomicAdd(A.tptr + m + A.colidx[e] + 1, 1);
+        }
+    __syncthreads();
+    {
+        __shared__ int carry;
+        if (tid == 0) carry = 0;
+        __syncthreads();
+        for (int base = 1; base <= N; base += kTT) {
+            const int idx = base + tid;
+            const int v = idx <= N ? A.tptr[idx] : 0;
+            int tot;
+            const int off = block_excl_scan(v, wsc, &tot);
+            if (idx <= N) A.tptr[idx] = carry + off + v;
+            __syncthreads();
+            if (tid == 0) carry += tot;
+            __syncthreads();
+        }
+    }
+    int *deg = reinterpret_cast<int *>(dyn);                                  // N ints
+    unsigned char *alive = dyn + 4 * (size_t)N;                               // N
+    unsigned char *sel = dyn + 5 * (size_t)N;                                 // N
+    for (int v = tid; v < N; v += kTT) deg[v] = 0;                            // fill cursor
+    if (tid == 0) A.ctr[2] = 0;
+    __syncthreads();
+    for (long long e = tid; e < nnz; e += kTT)
+        if (A.tmark[e]) {
+            const int u = A.erow[e], v = m + A.colidx[e];
+            const double w = A.val[e];
+            const int t = atomicAdd(A.ctr + 2, 1);
+            A.tei[t] = u;
+            A.tej[t] = v - m;
+            A.tval[t] = w;
+            const int pu = A.tptr[u] + atomicAdd(deg + u, 1);
+            const int pv = A.tptr[v] + atomicAdd(deg + v, 1);
+            A.tnbr[pu] = v;
+            A.tw[pu] = w;
+            A.tsrc[pu] = t;
+            A.tnbr[pv] = u;
+            A.tw[pv] = w;
+            A.tsrc[pv] = t;
+        }
+    for (int v = tid; v < N; v += kTT) {
+        alive[v] = 1;
+        A.dcur[v] = (v < m ? A.dr[v] : A.dc[v - m]) + mu;
+        A.hook[v] = v;                                                        // active list
+    }
+    if (tid == 0) {
+        A.ctr[0] = 0;
+        A.rstart[0] = 0;
+    }
+    __syncthreads();
+
+    // ---------------- 3. tree contraction = exact LDL^T of M_T ----------------
+    // active list ping-pong: A.hook (current) <-> A.comp (next)
+    int *act = A.hook, *nxt = A.comp;
+    int nact = N;
+    for (int round = 0; round < kTreeMaxRounds && nact > 0; ++round) {
+        for (int q = tid; q < nact; q += kTT) {
+            const int u = act[q];
+            unsigned char s0 = 0;
+            if (deg[u] <= 2) {
+                const unsigned pu = hash_prio(u, round);
+                s0 = 1;
+                for (int k = A.tptr[u]; k < A.tptr[u + 1]; ++k) {
+                    const int v = A.tnbr[k];
+                    if (v < 0 || !alive[v] || deg[v] > 2) continue;
+                    const unsigned pv = hash_prio(v, round);
+                    if (pv < pu || (pv == pu && v < u)) { s0 = 0; break; }
+                }
+            }
+            sel[u] = s0;
+        }
+        __syncthreads();
+        for (int q = tid; q < nact; q += kTT) {
+            const int u = act[q];
+            if (!sel[u]) continue;
+            int v1 = -1, v2 = -1, s1 = 0, s2 = 0;
+            double w1 = 0.0, w2 = 0.0;
+            for (int k = A.tptr[u]; k < A.tptr[u + 1]; ++k) {
+                const int v = A.tnbr[k];
+                if (v < 0) continue;
+                if (v1 < 0) { v1 = v; w1 = A.tw[k]; s1 = A.tsrc[k]; }
+                else { v2 = v; w2 = A.tw[k]; s2 = A.tsrc[k]; }
+            }
+            const double inv = 1.0 / A.dcur[u];
+            const int pos = atomicAdd(A.ctr + 0, 1);
+            A.fu[pos] = u;
+            A.fv1[pos] = v1;
+            A.fv2[pos] = v2;
+            A.fs1[pos] = s1;
+            A.fs2[pos] = s2;
+            A.fw1[pos] = w1;
+            A.fw2[pos] = w2;
+            A.fc1[pos] = w1 * inv;
+            A.fc2[pos] = w2 * inv;
+            A.finv[pos] = inv;
+            alive[u] = 0;
+            if (v1 >= 0) atomicAdd(A.dcur + v1, -w1 * w1 * inv);
+            if (v2 >= 0) atomicAdd(A.dcur + v2, -w2 * w2 * inv);
+            if (v2 < 0 && v1 >= 0) {          // rake: drop u from v1's list
+                for (int k = A.tptr[v1]; k < A.tptr[v1 + 1]; ++k)
+                    if (A.tnbr[k] == u) { A.tnbr[k] = -1; break; }
+                atomicSub(deg + v1, 1);
+            } else if (v2 >= 0) {             // compress: v1 -- v2 with the fill weight
+                const double wf = -w1 * w2 * inv;
+                for (int k = A.tptr[v1]; k < A.tptr[v1 + 1]; ++k)
+                    if (A.tnbr[k] == u) { A.tnbr[k] = v2; A.tw[k] = wf; A.tsrc[k] = -(pos + 1); break; }
+                for (int k = A.tptr[v2]; k < A.tptr[v2 + 1]; ++k)
+                    if (A.tnbr[k] == u) { A.tnbr[k] = v1; A.tw[k] = wf; A.tsrc[k] = -(pos + 1); break; }
+            }
+        }
+        __syncthreads();
+        // compact the active list (order-preserving): thread t owns act[q0, q0 + per)
+        const int per = (nact + kTT - 1) / kTT;
+        const int q0 = tid * per;
+        int nk = 0;
+        for (int j = 0; j < per; ++j) {
+            const int qq = q0 + j;
+            nk += (qq < nact && alive[act[qq]]) ? 1 : 0;
+        }
+        int tot;
+        int o = block_excl_scan(nk, wsc, &tot);
+        for (int j = 0; j < per; ++j) {
+            const int qq = q0 + j;
+            if (qq < nact && alive[act[qq]]) nxt[o++] = act[qq];
+        }
+        __syncthreads();
+        if (tid == 0) A.rstart[round + 1] = A.ctr[0];
+        int *t = act; act = nxt; nxt = t;
+        nact = tot;
+        nrounds = round + 1;
+        __syncthreads();
+    }
+    if (tid == 0) A.ctr[1] = nrounds;
+    }   // rebuild
+    t_fac = clock64() - t_start - t_mst;
+
+    // ---------------- 4. PCG on M with z = M_T^-1 r ----------------
+    double *vs = reinterpret_cast<double *>(dyn);                             // N doubles
+    // the late (small) rounds are latency-bound: keep their factor records in
+    // shared memory after the vector (budget from the launch), from round R0 on
+    struct Rec { int u, v1, v2, pad; double c1, c2, inv; };
+    Rec *tail = reinterpret_cast<Rec *>(dyn + 8 * (size_t)N);
+    const int tail_cap = A.tail_cap;
+    int R0 = nrounds;
+    while (R0 > 0 && A.rstart[nrounds] - A.rstart[R0 - 1] <= tail_cap) --R0;
+    const int tbase = A.rstart[R0];
+    for (int qq = tbase + tid; qq < A.rstart[nrounds]; qq += kTT) {
+        Rec rc;
+        rc.u = A.fu[qq]; rc.v1 = A.fv1[qq]; rc.v2 = A.fv2[qq]; rc.pad = 0;
+        rc.c1 = A.fc1[qq]; rc.c2 = A.fc2[qq]; rc.inv = A.finv[qq];
+        tail[qq - tbase] = rc;
+    }
+    __syncthreads();
+    const long long *rp = A.rowptr, *cp = A.colptr;
+    auto apply_M = [&](const double *src, double *dst) {
+        for (int k = tid; k < N; k += kTT) vs[k] = src[k];
+        __syncthreads();
+        for (int k0 = tid; k0 < N; k0 += 4 * kTT) {        // 4 independent rows per thread
+            long long b_[4], e_[4];
+            double s_[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = k0 + j * kTT;
+                b_[j] = e_[j] = 0;
+                s_[j] = 0.0;
+                if (k < m) { b_[j] = rp[k]; e_[j] = rp[k + 1]; s_[j] = (A.dr[k] + mu) * vs[k]; }
+                else if (k < N) { b_[j] = cp[k - m]; e_[j] = cp[k - m + 1]; s_[j] = (A.dc[k - m] + mu) * vs[k]; }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = k0 + j * kTT;
+                if (k >= N) continue;
+                double s = s_[j];
+                if (k < m)
+                    for (long long e = b_[j]; e < e_[j]; ++e) s = fma(A.val[e], vs[m + A.colidx[e]], s);
+                else
+                    for (long long e = b_[j]; e < e_[j]; ++e) s = fma(A.valT[e], vs[A.rowidx[e]], s);
+                dst[k] = s;
+            }
+        }
+    };
+    auto precond = [&](const double *src, double *dst) {
+        for (int k = tid; k < N; k += kTT) vs[k] = src[k];
+        __syncthreads();
+        for (int rr = 0; rr < nrounds; ++rr) {           // forward elimination
+            const int q1 = A.rstart[rr + 1];
+            if (rr < R0) {
+                for (int q = A.rstart[rr] + tid; q < q1; q += kTT) {
+                    const double yu = vs[A.fu[q]];
+                    const int v1 = A.fv1[q], v2 = A.fv2[q];
+                    if (v1 >= 0) sm_add(vs + v1, -A.fc1[q] * yu);
+                    if (v2 >= 0) sm_add(vs + v2, -A.fc2[q] * yu);
+                }
+            } else {
+                for (int q = A.rstart[rr] + tid; q < q1; q += kTT) {
+                    const Rec rc = tail[q - tbase];
+                    const double yu = vs[rc.u];
+                    if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
+                    if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+                }
+            }
+            __syncthreads();
+        }
+        for (int rr = nrounds - 1; rr >= 0; --rr) {      // back substitution
+            const int q1 = A.rstart[rr + 1];
+            if (rr < R0) {
+                for (int q = A.rstart[rr] + tid; q < q1; q += kTT) {
+                    const int u = A.fu[q];
+                    const int v1 = A.fv1[q], v2 = A.fv2[q];
+                    double xu = vs[u] * A.finv[q];
+                    if (v1 >= 0) xu = fma(-A.fc1[q], vs[v1], xu);
+                    if (v2 >= 0) xu = fma(-A.fc2[q], vs[v2], xu);
+                    vs[u] = xu;
+                }
+            } else {
+                for (int q = A.rstart[rr] + tid; q < q1; q += kTT) {
+                    const Rec rc = tail[q - tbase];
+                    double xu = vs[rc.u] * rc.inv;
+                    if (rc.v1 >= 0) xu = fma(-rc.c1, vs[rc.v1], xu);
+                    if (rc.v2 >= 0) xu = fma(-rc.c2, vs[rc.v2], xu);
+                    vs[rc.u] = xu;
+                }
+            }
+            __syncthreads();
+        }
+        for (int k = tid; k < N; k += kTT) dst[k] = vs[k];
+    };
+    double *x = A.x, *r = A.r, *z = A.z, *p = A.p, *q = A.q;
+    double l_bb = 0.0;
+    for (int k = tid; k < N; k += kTT) {
+        const double b = A.rhs[k];
+        x[k] = 0.0;
+        r[k] = b;
+        l_bb = fma(b, b, l_bb);
+    }
+    __syncthreads();
+    const double bb = tree_block_sum(l_bb, red);
+    double rr2 = bb;
+    int it = 0;
+    double relres = bb > 0.0 ? 1.0 : 0.0;
+    double rz = 0.0;
+    if (bb > 0.0) {
+        const long long tp0 = clock64();
+        precond(r, z);
+        __syncthreads();
+        t_pc += clock64() - tp0;
+        double l = 0.0;
+        for (int k = tid; k < N; k += kTT) {
+            p[k] = z[k];
+            l = fma(r[k], z[k], l);
+        }
+        rz = tree_block_sum(l, red);
+    }
+    while (bb > 0.0) {
+        relres = sqrt(rr2 / bb);
+        if (relres <= A.rtol || it >= A.maxit) break;
+        __syncthreads();
+        const long long tm0 = clock64();
+        apply_M(p, q);
+        __syncthreads();
+        t_mv += clock64() - tm0;
+        double l = 0.0;
+        for (int k = tid; k < N; k += kTT) l = fma(p[k], q[k], l);
+        const double pq = tree_block_sum(l, red);
+        if (!(pq > 0.0)) break;
+        const double alpha = rz / pq;
+        double l2 = 0.0;
+        for (int k = tid; k < N; k += kTT) {
+            x[k] = fma(alpha, p[k], x[k]);
+            const double rv = fma(-alpha, q[k], r[k]);
+            r[k] = rv;
+            l2 = fma(rv, rv, l2);
+        }
+        rr2 = tree_block_sum(l2, red);
+        ++it;
+        if (sqrt(rr2 / bb) <= A.rtol || it >= A.maxit) { relres = sqrt(rr2 / bb); break; }
+        const long long tp0 = clock64();
+        precond(r, z);
+        __syncthreads();
+        t_pc += clock64() - tp0;
+        double l3 = 0.0;
+        for (int k = tid; k < N; k += kTT) l3 = fma(r[k], z[k], l3);
+        const double rz2 = tree_block_sum(l3, red);
+        const double beta = rz2 / rz;
+        rz = rz2;
+        for (int k = tid; k < N; k += kTT) p[k] = fma(beta, p[k], z[k]);
+    }
+    __syncthreads();
+    double l_s = 0.0, l_a = 0.0;
+    if (A.gradf) {
+        for (int k = tid; k < N; k += kTT) {
+            const double xv = x[k];
+            if (k < m) {
+                l_s = fma(A.gradf[k], xv, l_s);
+                l_a = fma(A.a[k], xv, l_a);
+            } else {
+                l_s = fma(A.gradg[k - m], xv, l_s);
+                l_a = fma(A.b[k - m], xv, l_a);
+            }
+        }
+    }
+    const double S = tree_block_sum(l_s, red);
+    const double AD = tree_block_sum(l_a, red);
+    if (tid == 0) {
+        A.st[0] = (double)it;
+        A.st[1] = relres;
+        A.st[2] = S;
+        A.st[3] = AD;
+        A.st[4] = (double)nrounds;
+        A.st[5] = (double)(A.tptr[N] / 2);
+        A.st[6] = (double)t_mst;
+        A.st[7] = (double)t_fac;
+        A.st[8] = (double)t_pc;
+        A.st[9] = (double)t_mv;
+        A.st[10] = (double)(clock64() - t_start);
+        A.st[11] = rebuilt ? 1.0 : 0.0;
+    }
+}
+
+}  // namespace pins

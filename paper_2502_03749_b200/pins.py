@@ -22,7 +22,7 @@ EXPORTS = [
     "pins_default_params", "pins_workspace_create", "pins_workspace_destroy", "pins_last_error",
     "pins_center_init", "pins_center_update", "pins_sinkhorn_sweep", "pins_evaluate",
     "pins_get_csr", "pins_sparsify_dense", "pins_cg", "pins_newton_step", "pins_residuals", "pins_plan", "pins_solve",
-    "pins_prof_enable", "pins_prof_reset", "pins_prof_read", "pins_solve_host",
+    "pins_prof_enable", "pins_prof_reset", "pins_prof_read", "pins_prof_read_work", "pins_solve_host",
 ]
 
 
@@ -83,6 +83,7 @@ def load():
         "pins_prof_enable": (None, [I32]),
         "pins_prof_reset": (None, []),
         "pins_prof_read": (I32, [I32, POINTER(I64), POINTER(D)]),
+        "pins_prof_read_work": (I32, [I32, POINTER(D)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -294,7 +295,9 @@ def prof_read() -> Dict[str, Dict]:
     for c, name in enumerate(PROF_CLASSES):
         n, ms = c_int64(), c_double()
         _check(lib.pins_prof_read(c, ctypes.byref(n), ctypes.byref(ms)))
-        out[name] = {"launches": n.value, "ms": ms.value}
+        wk = c_double()
+        _check(lib.pins_prof_read_work(c, ctypes.byref(wk)))
+        out[name] = {"launches": n.value, "ms": ms.value, "work": wk.value}
     return out
 
 

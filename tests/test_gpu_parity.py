@@ -202,8 +202,12 @@ def test_cg_against_direct_solve(P):
     np.testing.assert_allclose(H(x), x_ref, rtol=1e-6, atol=1e-9 * np.abs(x_ref).max())
 
 
+@pytest.mark.parametrize("cg", ["tree", "cluster", "grid"])
 @pytest.mark.parametrize("name,mk", CASES[:5])
-def test_newton_step(P, name, mk):
+def test_newton_step(P, name, mk, cg, monkeypatch):
+    # the three Newton-system solvers: spanning-tree PCG (one CTA),
+    # Jacobi-Schur CG (one cluster), Jacobi CG on the full system (cooperative grid)
+    monkeypatch.setenv("PINS_CG", cg)
     w = mk()
     C, Ck, phi, psi, s, f, g = oracle_state(w, 2)
     # start away from the subproblem optimum: one plain sweep from the warm start
