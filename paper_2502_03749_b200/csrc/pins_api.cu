@@ -1148,6 +1148,9 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
         for (int q = 0; q < 7; ++q) acc[q] += hs[4 + q];
         acc[7] += hs[11];
         ++calls;
+        if (calls % 200 == 1 || getenv("PINS_TREE_STATS")[0] == '2')
+            fprintf(stderr, "  last call: its %.0f rebuilt %.0f | kcycles mst %.1f fac %.1f pc %.1f mv %.1f total %.1f\n",
+                    cg_its, hs[11], hs[6] / 1e3, hs[7] / 1e3, hs[8] / 1e3, hs[9] / 1e3, hs[10] / 1e3);
         if (calls % 200 == 1)
             fprintf(stderr, "tree-cg calls %ld nnz %lld its %.0f rebuilds %.0f | Mcycles mst %.1f fac %.1f pc %.1f mv %.1f total %.1f\n",
                     calls, ws->nnz, cg_its, acc[7], acc[2] / 1e6, acc[3] / 1e6, acc[4] / 1e6, acc[5] / 1e6, acc[6] / 1e6);

@@ -109,6 +109,15 @@ struct PassArgs {
     const double *a_dot, *f_dot, *b_dot, *g_dot;   // SUM: <a,f> + <b,g> (global finalize)
 };
 
+// Conservative fp32 form of the skip test  x = q - w D > thr  (phase 1 of a chunk):
+// qs = q rounded up by 2^-20 |q|, w_lo = w (1 - 2^-19), thr_lo = thr - 2^-20 |thr|;
+// fmaf(-w_lo, D, qs) > thr_lo holds whenever the fp64 test does (the margins cover
+// every fp32 rounding), so no entry the fp64 test keeps is skipped (R10).
+__device__ __forceinline__ float qs_of(double q) {
+    return q == -INFINITY ? -INFINITY : (float)(q + fabs(q) * 0x1p-20);
+}
+__device__ __forceinline__ float thr_lo_of(double t) { return (float)(t - fabs(t) * 0x1p-20 - 0x1p-30); }
+
 // exact potential expressions (no FMA contraction: identical bits in both orientations)
 __device__ __forceinline__ double pot_q(double g, double psi, double inv_eta) {
     return __dmul_rn(__dadd_rn(g, psi), inv_eta);
@@ -129,6 +138,7 @@ struct Buf {
     double q[kCC];                               // column potential
     double qt[kCC];                              // skip-test column value (q + trial bump)
     double ev[kCC];                              // trial factor
+    float qs[kCC];                               // fp32 skip-test value: qt rounded up by 2^-20 |qt|
     float ny[kCC];
     alignas(16) float y32[PTS32 ? kCC * DP : 4];
     double y64[PTS64 ? kCC * DP : 1];
@@ -197,7 +207,10 @@ struct Pref {
             double q = -INFINITY;
             if (tid < nc) q = qmode ? pot_p(g, psi, inv_eta) : pot_q(g, psi, inv_eta);
             B.q[tid] = q;
-            if (!trial) B.qt[tid] = q;
+            if (!trial) {
+                B.qt[tid] = q;
+                B.qs[tid] = qs_of(q);
+            }
         } else if (tid < 2 * kCC && trial) {
             B.ev[tid - kCC] = ev;
         }
@@ -235,7 +248,9 @@ struct Pref {
         const int tid = threadIdx.x;
         if (tid >= kCC && tid < 2 * kCC) {
             const int c = tid - kCC;
-            B.qt[c] = B.q[c] + bv;
+            const double qt = B.q[c] + bv;
+            B.qt[c] = qt;
+            B.qs[c] = qs_of(qt);
         }
     }
 };
@@ -512,6 +527,7 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
     RowPt<COST, DP> rp;
     rp.load(P, i, valid);
     const double w = A.w, inv_eta = A.inv_eta;
+    const float w_lo = (float)w * (1.f - 0x1p-19f);
     double mx = -INFINITY, sm = 0.0;
     int jm = -1;
     if (valid) {
@@ -526,20 +542,18 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
                              [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
         if (!valid) return;
         // phase 1 (branch-free): skip test against the chunk-start bound of the row max
-        const double thr = mx - kLseCut;
+        const float thr32 = thr_lo_of(mx - kLseCut);
         unsigned mask = 0u;
 #pragma unroll
         for (int c = 0; c < kCC; ++c) {
-            double D;
+            float Df;
             if constexpr (COST == PC_SQTC) {
-                const float Df = fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
+                Df = fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
                 dsc[c] = Df;
-                D = (double)Df;
             } else {
-                D = chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+                Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c);
             }
-            const double x = fma(-w, D, B.q[c]);
-            mask |= (c < nc && x > thr) ? (1u << c) : 0u;
+            mask |= (c < nc && fmaf(-w_lo, Df, B.qs[c]) > thr32) ? (1u << c) : 0u;
         }
         // phase 2: the surviving entries of this row, in column order (one exp each)
         while (mask) {
@@ -647,6 +661,8 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
     // only formed for entries that pass (R10); near the cut the two orientations may
     // decide differently, which changes sums by < e^-80 and never the kept pattern
     const double thr = -kSumCut - Pi - bu;
+    const float thr32 = thr_lo_of(thr);
+    const float w_lo = (float)w * (1.f - 0x1p-19f);
     double acc = 0.0, cx = 0.0, em = 0.0, mz = -INFINITY;
     int cnt = 0;
     const long long bufbase = (i * P.S + sp) * P.cap;
@@ -657,15 +673,14 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
         unsigned mask = 0u;
 #pragma unroll
         for (int c = 0; c < kCC; ++c) {
-            double D;
+            float Df;
             if constexpr (COST == PC_SQTC) {
-                const float Df = fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
+                Df = fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
                 dsc[c] = Df;
-                D = (double)Df;
             } else {
-                D = chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+                Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c);
             }
-            mask |= (c < nc && fma(-w, D, B.qt[c]) > thr) ? (1u << c) : 0u;
+            mask |= (c < nc && fmaf(-w_lo, Df, B.qs[c]) > thr32) ? (1u << c) : 0u;
         }
         while (mask) {
             const int c = __ffs(mask) - 1;
