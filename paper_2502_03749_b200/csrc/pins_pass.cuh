@@ -24,7 +24,7 @@
 // plan of Eq. (7) is concentrated: Thm 4.3): in the LSE a
 // term is skipped when x < M_lo - kLseCut, where M_lo is a running lower
 // bound of the row maximum (seeded with the previous pass's argmax column),
-// so each skipped term is < e^-50 of the largest; in the sums an entry is
+// so each skipped term is < e^-36 of the largest; in the sums an entry is
 // skipped when z < -kSumCut (X~ < 1.8e-35).  DESIGN.md §5 bounds the effect.
 //
 // Reductions are deterministic: per (split, row) partials, merged in split
@@ -40,7 +40,7 @@ namespace pins {
 
 constexpr int kPT = 128;            // threads per CTA = pass rows per CTA
 constexpr int kCC = 32;             // columns per staged chunk
-constexpr double kLseCut = 50.0;
+constexpr double kLseCut = 36.0;
 constexpr double kSumCut = 80.0;
 
 // cost evaluation variants (host picks, see pins_api.cu choose_cost)

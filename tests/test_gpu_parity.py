@@ -278,13 +278,13 @@ BENCH = dict(K=20000, outer_rule=1, outer_tol=1e-7, newton_tol=1e-10)
 BENCH_A2 = dict(K=20000, outer_rule=1, outer_tol=1e-7, newton_tol=1e-8)   # bench.py BENCH_PARAMS
 
 
-@pytest.mark.parametrize("name,outer_tol", [("c0_pts64", 1e-7), ("c1_rand1k", 5e-8), ("c2_img4k", 1e-7),
+@pytest.mark.parametrize("name,outer_tol", [("c0_pts64", 1e-7), ("c1_rand1k", 2e-8), ("c2_img4k", 1e-7),
                                             ("c3_gmm10k", 1e-7), ("c4_l1rect", 1e-7)])
 def test_solve_full_size_reaches_exact_lp(P, name, outer_tol):
     # BASELINE.json full sizes, bench parameters (A.2 defaults + halving stop, reading R6):
     # KKT <= 1e-8 and the exact LP optimum of the oracle's network simplex to 1e-7.
     # c1 (dense uniform costs) has a long plateau in <C, X^k>: the halving estimator
-    # needs 5e-8 there
+    # needs 2e-8 there
     gold = json.load(open(os.path.join(GOLD, f"exact_{name}.json")))
     w = make(name)
     pb = P.DeviceProblem.from_workload(w)
