@@ -919,8 +919,9 @@ size_t cluster_cg_smem(long long m, long long n) {
     return sizeof(double) * (size_t)(8 * R + 2 * Cc) + sizeof(int) * (size_t)(2 * R + 2 * Cc + 2) + 16;
 }
 bool use_cluster_cg(pins_workspace *ws, long long m, long long n) {
-    return ws->nnz <= kClusterNnzMax && cluster_cg_smem(m, n) <= (size_t)kClusterSmem - 16 * 1024 &&
-           ws->csc_ready;
+    long long lim = kClusterNnzMax;
+    if (const char *e = getenv("PINS_CLUSTER_NNZ_MAX")) lim = atoll(e);   // experiments
+    return ws->nnz <= lim && cluster_cg_smem(m, n) <= (size_t)kClusterSmem - 16 * 1024 && ws->csc_ready;
 }
 
 // kept side = the smaller of (rows, columns); the other is eliminated exactly
@@ -1005,7 +1006,7 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     // comp hook tptr tnbr(2) deg fu fv1 fv2 tei tej tsrc(2) fs1 fs2 = 15 N, + rstart, ctr
     const long long ni_fixed = 15 * N + 1 + kTreeMaxRounds + 1 + 8;
     const long long ni = ni_fixed + nnz;
-    const long long nd = 2 * N + N + 3 * N + 4 * N + 3 * N;   // tw, dcur, fc1/fc2/finv, r z p q, tval fw1 fw2
+    const long long nd = 2 * N + N + 3 * N + 4 * N + 3 * N + 5 * N;   // tw, dcur, fc1/fc2/finv, r z p q, tval fw1 fw2, frec
     const void *old_i = ws->tr_i.p, *old_d = ws->tr_d.p;
     PINS_TRY(ensure(ws->tr_i, sizeof(int) * ni));
     PINS_TRY(ensure(ws->tr_d, sizeof(double) * nd));
@@ -1064,7 +1065,8 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     A.q = dp_; dp_ += N;
     A.tval = dp_; dp_ += N;
     A.fw1 = dp_; dp_ += N;
-    A.fw2 = dp_;
+    A.fw2 = dp_; dp_ += N;
+    A.frec = dp_;
     unsigned char *bp = ptr<unsigned char>(ws->tr_u8);
     A.alive = bp; bp += N;
     A.sel = bp; bp += N;

@@ -138,8 +138,8 @@ struct Buf {
     double q[kCC];                               // column potential
     double qt[kCC];                              // skip-test column value (q + trial bump)
     double ev[kCC];                              // trial factor
-    float qs[kCC];                               // fp32 skip-test value: qt rounded up by 2^-20 |qt|
-    float ny[kCC];
+    alignas(16) float qs[kCC];                   // fp32 skip-test value: qt rounded up by 2^-20 |qt|
+    alignas(16) float ny[kCC];
     alignas(16) float y32[PTS32 ? kCC * DP : 4];
     double y64[PTS64 ? kCC * DP : 1];
     alignas(128) unsigned char yh[COST == PC_SQTC ? kCC * 32 : 16];   // UMMA B tile (kCC x 16 fp16)
@@ -544,16 +544,35 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
         // phase 1 (branch-free): skip test against the chunk-start bound of the row max
         const float thr32 = thr_lo_of(mx - kLseCut);
         unsigned mask = 0u;
+        float Dv[COST == PC_SQTC ? kCC : 1];
 #pragma unroll
-        for (int c = 0; c < kCC; ++c) {
-            float Df;
+        for (int c4 = 0; c4 < kCC; c4 += 4) {
+            const float4 qs4 = *reinterpret_cast<const float4 *>(B.qs + c4);
+            const float qsv[4] = {qs4.x, qs4.y, qs4.z, qs4.w};
+            float nyv[4] = {0.f, 0.f, 0.f, 0.f};
             if constexpr (COST == PC_SQTC) {
-                Df = fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
-                dsc[c] = Df;
-            } else {
-                Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+                const float4 ny4 = *reinterpret_cast<const float4 *>(B.ny + c4);
+                nyv[0] = ny4.x; nyv[1] = ny4.y; nyv[2] = ny4.z; nyv[3] = ny4.w;
             }
-            mask |= (c < nc && fmaf(-w_lo, Df, B.qs[c]) > thr32) ? (1u << c) : 0u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = c4 + j;
+                float Df;
+                if constexpr (COST == PC_SQTC) {
+                    Df = fmaf(-2.f, dots[c], rp.nx + nyv[j]);
+                    Dv[c] = Df;
+                } else {
+                    Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+                }
+                mask |= (c < nc && fmaf(-w_lo, Df, qsv[j]) > thr32) ? (1u << c) : 0u;
+            }
+        }
+        if constexpr (COST == PC_SQTC) {
+            // distances are needed only where some lane of the warp has a survivor
+            if (__any_sync(__activemask(), mask != 0u)) {
+#pragma unroll
+                for (int c = 0; c < kCC; ++c) dsc[c] = Dv[c];
+            }
         }
         // phase 2: the surviving entries of this row, in column order (one exp each)
         while (mask) {
@@ -671,16 +690,35 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
                              [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
         if (!valid) return;
         unsigned mask = 0u;
+        float Dv[COST == PC_SQTC ? kCC : 1];
 #pragma unroll
-        for (int c = 0; c < kCC; ++c) {
-            float Df;
+        for (int c4 = 0; c4 < kCC; c4 += 4) {
+            const float4 qs4 = *reinterpret_cast<const float4 *>(B.qs + c4);
+            const float qsv[4] = {qs4.x, qs4.y, qs4.z, qs4.w};
+            float nyv[4] = {0.f, 0.f, 0.f, 0.f};
             if constexpr (COST == PC_SQTC) {
-                Df = fmaf(-2.f, dots[c], rp.nx + B.ny[c]);
-                dsc[c] = Df;
-            } else {
-                Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+                const float4 ny4 = *reinterpret_cast<const float4 *>(B.ny + c4);
+                nyv[0] = ny4.x; nyv[1] = ny4.y; nyv[2] = ny4.z; nyv[3] = ny4.w;
             }
-            mask |= (c < nc && fmaf(-w_lo, Df, B.qs[c]) > thr32) ? (1u << c) : 0u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = c4 + j;
+                float Df;
+                if constexpr (COST == PC_SQTC) {
+                    Df = fmaf(-2.f, dots[c], rp.nx + nyv[j]);
+                    Dv[c] = Df;
+                } else {
+                    Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+                }
+                mask |= (c < nc && fmaf(-w_lo, Df, qsv[j]) > thr32) ? (1u << c) : 0u;
+            }
+        }
+        if constexpr (COST == PC_SQTC) {
+            // distances are needed only where some lane of the warp has a survivor
+            if (__any_sync(__activemask(), mask != 0u)) {
+#pragma unroll
+                for (int c = 0; c < kCC; ++c) dsc[c] = Dv[c];
+            }
         }
         while (mask) {
             const int c = __ffs(mask) - 1;
@@ -897,8 +935,10 @@ __global__ void __launch_bounds__(kPT) csr_build_kernel(PassSide P0, PassSide P1
     const int tid = threadIdx.x;
     const long long i = (long long)rb * kPT + tid;
     long long tot = 0;
-    if (i < P.M)
+    if (i < P.M) {
+#pragma unroll 8
         for (int s = 0; s < P.S; ++s) tot += min((long long)P.cnt[i * P.S + s], P.cap);
+    }
     sc[tid] = tot;
     __syncthreads();
     for (int o = 1; o < kPT; o <<= 1) {
@@ -911,14 +951,20 @@ __global__ void __launch_bounds__(kPT) csr_build_kernel(PassSide P0, PassSide P1
     if (i < P.M) {
         O.ptr[i] = start;
         long long dst = start;
-        for (int s = 0; s < P.S; ++s) {
-            const long long len = min((long long)P.cnt[i * P.S + s], P.cap);
-            const long long src = (i * P.S + s) * P.cap;
-            for (long long k = 0; k < len; ++k) {
-                O.idx[dst + k] = P.bcol[src + k];
-                O.val[dst + k] = P.bval[src + k];
+        for (int s0 = 0; s0 < P.S; s0 += 8) {          // counts of 8 splits in flight
+            int len[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                len[j] = s0 + j < P.S ? (int)min((long long)P.cnt[i * P.S + s0 + j], P.cap) : 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const long long src = (i * P.S + s0 + j) * P.cap;
+                for (int k = 0; k < len[j]; ++k) {
+                    O.idx[dst + k] = P.bcol[src + k];
+                    O.val[dst + k] = P.bval[src + k];
+                }
+                dst += len[j];
             }
-            dst += len;
         }
         if (i == P.M - 1) O.ptr[P.M] = dst;
     }

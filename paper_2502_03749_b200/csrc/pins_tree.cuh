@@ -66,7 +66,8 @@ struct TreeArgs {
     int *fu, *fv1, *fv2;               // [N] factor in elimination order
     double *fc1, *fc2, *finv;          // [N]
     int *rstart;                       // [kTreeMaxRounds + 1]
-    double *r, *z, *p, *q;             // [N] CG vectors
+    double *r, *z, *p, *q;             // [N] CG vectors (z unused: kept in shared memory)
+    double *frec;                      // [5 N] packed factor records (40 B each)
     int *ctr;                          // [8] counters: [0] records [1] rounds [2] tree edges [3] valid
     int tail_cap;                      // factor records cached in shared memory
     // reuse across Newton steps: tree edge list, slot sources, weights
@@ -401,26 +402,116 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
 
     // ---------------- 4. PCG on M with z = M_T^-1 r ----------------
     double *vs = reinterpret_cast<double *>(dyn);                             // N doubles
-    // the late (small) rounds are latency-bound: keep their factor records in
-    // shared memory after the vector (budget from the launch), from round R0 on
+    // factor records packed (one 40-byte load per eliminated node); the late
+    // (small) rounds are latency-bound, so their records also go to shared memory
     struct Rec { int u, v1, v2, pad; double c1, c2, inv; };
-    Rec *tail = reinterpret_cast<Rec *>(dyn + 8 * (size_t)N);
-    const int tail_cap = A.tail_cap;
-    int R0 = nrounds;
-    while (R0 > 0 && A.rstart[nrounds] - A.rstart[R0 - 1] <= tail_cap) --R0;
-    const int tbase = A.rstart[R0];
-    for (int qq = tbase + tid; qq < A.rstart[nrounds]; qq += kTT) {
+    Rec *frec = reinterpret_cast<Rec *>(A.frec);
+    const int nrec = A.rstart[nrounds];
+    for (int qq = tid; qq < nrec; qq += kTT) {
         Rec rc;
         rc.u = A.fu[qq]; rc.v1 = A.fv1[qq]; rc.v2 = A.fv2[qq]; rc.pad = 0;
         rc.c1 = A.fc1[qq]; rc.c2 = A.fc2[qq]; rc.inv = A.finv[qq];
-        tail[qq - tbase] = rc;
+        frec[qq] = rc;
     }
+    Rec *tail = reinterpret_cast<Rec *>(dyn + 8 * (size_t)N);
+    const int tail_cap = A.tail_cap;
+    int R0 = nrounds;
+    while (R0 > 0 && nrec - A.rstart[R0 - 1] <= tail_cap) --R0;
+    const int tbase = A.rstart[R0];
     __syncthreads();
-    const long long *rp = A.rowptr, *cp = A.colptr;
-    auto apply_M = [&](const double *src, double *dst) {
-        for (int k = tid; k < N; k += kTT) vs[k] = src[k];
+    for (int qq = tbase + tid; qq < nrec; qq += kTT) tail[qq - tbase] = frec[qq];
+    __syncthreads();
+    // the suffix of rounds with <= 32 records each is run by warp 0 alone, with
+    // __syncwarp between rounds instead of a CTA barrier
+    int RW = nrounds;
+    while (RW > R0 && A.rstart[RW] - A.rstart[RW - 1] <= 32) --RW;
+    const int warp_id = tid >> 5, lane_id = tid & 31;
+    // in place on vs: forward elimination then back substitution (vs: r -> z)
+    auto precond_inplace = [&]() {
+        for (int rr = 0; rr < RW; ++rr) {
+            const int q0r = A.rstart[rr], q1 = A.rstart[rr + 1];
+            const Rec *src = rr < R0 ? frec : tail - tbase;
+            for (int q = q0r + tid; q < q1; q += kTT) {
+                const Rec rc = src[q];
+                const double yu = vs[rc.u];
+                if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
+                if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+            }
+            __syncthreads();
+        }
+        if (warp_id == 0) {
+            const Rec *src = tail - tbase;
+            for (int rr = RW; rr < nrounds; ++rr) {
+                const int q = A.rstart[rr] + lane_id;
+                if (q < A.rstart[rr + 1]) {
+                    const Rec rc = src[q];
+                    const double yu = vs[rc.u];
+                    if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
+                    if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+                }
+                __syncwarp();
+            }
+            for (int rr = nrounds - 1; rr >= RW; --rr) {
+                const int q = A.rstart[rr] + lane_id;
+                if (q < A.rstart[rr + 1]) {
+                    const Rec rc = src[q];
+                    double xu = vs[rc.u] * rc.inv;
+                    if (rc.v1 >= 0) xu = fma(-rc.c1, vs[rc.v1], xu);
+                    if (rc.v2 >= 0) xu = fma(-rc.c2, vs[rc.v2], xu);
+                    vs[rc.u] = xu;
+                }
+                __syncwarp();
+            }
+        }
         __syncthreads();
-        for (int k0 = tid; k0 < N; k0 += 4 * kTT) {        // 4 independent rows per thread
+        for (int rr = RW - 1; rr >= 0; --rr) {
+            const int q0r = A.rstart[rr], q1 = A.rstart[rr + 1];
+            const Rec *src = rr < R0 ? frec : tail - tbase;
+            for (int q = q0r + tid; q < q1; q += kTT) {
+                const Rec rc = src[q];
+                double xu = vs[rc.u] * rc.inv;
+                if (rc.v1 >= 0) xu = fma(-rc.c1, vs[rc.v1], xu);
+                if (rc.v2 >= 0) xu = fma(-rc.c2, vs[rc.v2], xu);
+                vs[rc.u] = xu;
+            }
+            __syncthreads();
+        }
+    };
+    const long long *rp = A.rowptr, *cp = A.colptr;
+    double *x = A.x, *r = A.r, *p = A.p, *q = A.q;
+    // init: x = 0, r = b; z = M_T^-1 r (in vs); p = z (global and in vs)
+    double l_bb = 0.0;
+    for (int k = tid; k < N; k += kTT) {
+        const double bk = A.rhs[k];
+        x[k] = 0.0;
+        r[k] = bk;
+        vs[k] = bk;
+        l_bb = fma(bk, bk, l_bb);
+    }
+    const double bb = tree_block_sum(l_bb, red);     // (synchronises)
+    double rr2 = bb;
+    int it = 0;
+    double relres = bb > 0.0 ? 1.0 : 0.0;
+    double rz = 0.0;
+    if (bb > 0.0) {
+        const long long tp0 = clock64();
+        precond_inplace();
+        t_pc += clock64() - tp0;
+        double l = 0.0;
+        for (int k = tid; k < N; k += kTT) {
+            const double zk = vs[k];
+            p[k] = zk;
+            l = fma(r[k], zk, l);
+        }
+        rz = tree_block_sum(l, red);
+    }
+    while (bb > 0.0) {
+        relres = sqrt(rr2 / bb);
+        if (relres <= A.rtol || it >= A.maxit) break;
+        // q = M p (p in vs), fused <p, q>
+        const long long tm0 = clock64();
+        double l = 0.0;
+        for (int k0 = tid; k0 < N; k0 += 4 * kTT) {
             long long b_[4], e_[4];
             double s_[4];
 #pragma unroll
@@ -435,120 +526,45 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
             for (int j = 0; j < 4; ++j) {
                 const int k = k0 + j * kTT;
                 if (k >= N) continue;
-                double s = s_[j];
+                double sv = s_[j];
                 if (k < m)
-                    for (long long e = b_[j]; e < e_[j]; ++e) s = fma(A.val[e], vs[m + A.colidx[e]], s);
+                    for (long long e = b_[j]; e < e_[j]; ++e) sv = fma(A.val[e], vs[m + A.colidx[e]], sv);
                 else
-                    for (long long e = b_[j]; e < e_[j]; ++e) s = fma(A.valT[e], vs[A.rowidx[e]], s);
-                dst[k] = s;
+                    for (long long e = b_[j]; e < e_[j]; ++e) sv = fma(A.valT[e], vs[A.rowidx[e]], sv);
+                q[k] = sv;
+                l = fma(vs[k], sv, l);
             }
         }
-    };
-    auto precond = [&](const double *src, double *dst) {
-        for (int k = tid; k < N; k += kTT) vs[k] = src[k];
-        __syncthreads();
-        for (int rr = 0; rr < nrounds; ++rr) {           // forward elimination
-            const int q1 = A.rstart[rr + 1];
-            if (rr < R0) {
-                for (int q = A.rstart[rr] + tid; q < q1; q += kTT) {
-                    const double yu = vs[A.fu[q]];
-                    const int v1 = A.fv1[q], v2 = A.fv2[q];
-                    if (v1 >= 0) sm_add(vs + v1, -A.fc1[q] * yu);
-                    if (v2 >= 0) sm_add(vs + v2, -A.fc2[q] * yu);
-                }
-            } else {
-                for (int q = A.rstart[rr] + tid; q < q1; q += kTT) {
-                    const Rec rc = tail[q - tbase];
-                    const double yu = vs[rc.u];
-                    if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
-                    if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
-                }
-            }
-            __syncthreads();
-        }
-        for (int rr = nrounds - 1; rr >= 0; --rr) {      // back substitution
-            const int q1 = A.rstart[rr + 1];
-            if (rr < R0) {
-                for (int q = A.rstart[rr] + tid; q < q1; q += kTT) {
-                    const int u = A.fu[q];
-                    const int v1 = A.fv1[q], v2 = A.fv2[q];
-                    double xu = vs[u] * A.finv[q];
-                    if (v1 >= 0) xu = fma(-A.fc1[q], vs[v1], xu);
-                    if (v2 >= 0) xu = fma(-A.fc2[q], vs[v2], xu);
-                    vs[u] = xu;
-                }
-            } else {
-                for (int q = A.rstart[rr] + tid; q < q1; q += kTT) {
-                    const Rec rc = tail[q - tbase];
-                    double xu = vs[rc.u] * rc.inv;
-                    if (rc.v1 >= 0) xu = fma(-rc.c1, vs[rc.v1], xu);
-                    if (rc.v2 >= 0) xu = fma(-rc.c2, vs[rc.v2], xu);
-                    vs[rc.u] = xu;
-                }
-            }
-            __syncthreads();
-        }
-        for (int k = tid; k < N; k += kTT) dst[k] = vs[k];
-    };
-    double *x = A.x, *r = A.r, *z = A.z, *p = A.p, *q = A.q;
-    double l_bb = 0.0;
-    for (int k = tid; k < N; k += kTT) {
-        const double b = A.rhs[k];
-        x[k] = 0.0;
-        r[k] = b;
-        l_bb = fma(b, b, l_bb);
-    }
-    __syncthreads();
-    const double bb = tree_block_sum(l_bb, red);
-    double rr2 = bb;
-    int it = 0;
-    double relres = bb > 0.0 ? 1.0 : 0.0;
-    double rz = 0.0;
-    if (bb > 0.0) {
-        const long long tp0 = clock64();
-        precond(r, z);
-        __syncthreads();
-        t_pc += clock64() - tp0;
-        double l = 0.0;
-        for (int k = tid; k < N; k += kTT) {
-            p[k] = z[k];
-            l = fma(r[k], z[k], l);
-        }
-        rz = tree_block_sum(l, red);
-    }
-    while (bb > 0.0) {
-        relres = sqrt(rr2 / bb);
-        if (relres <= A.rtol || it >= A.maxit) break;
-        __syncthreads();
-        const long long tm0 = clock64();
-        apply_M(p, q);
-        __syncthreads();
-        t_mv += clock64() - tm0;
-        double l = 0.0;
-        for (int k = tid; k < N; k += kTT) l = fma(p[k], q[k], l);
         const double pq = tree_block_sum(l, red);
+        t_mv += clock64() - tm0;
         if (!(pq > 0.0)) break;
         const double alpha = rz / pq;
+        // x += alpha p, r -= alpha q, ||r||^2; stage r into vs for the preconditioner
         double l2 = 0.0;
         for (int k = tid; k < N; k += kTT) {
-            x[k] = fma(alpha, p[k], x[k]);
+            x[k] = fma(alpha, vs[k], x[k]);
             const double rv = fma(-alpha, q[k], r[k]);
             r[k] = rv;
+            vs[k] = rv;
             l2 = fma(rv, rv, l2);
         }
         rr2 = tree_block_sum(l2, red);
         ++it;
         if (sqrt(rr2 / bb) <= A.rtol || it >= A.maxit) { relres = sqrt(rr2 / bb); break; }
         const long long tp0 = clock64();
-        precond(r, z);
-        __syncthreads();
+        precond_inplace();
         t_pc += clock64() - tp0;
         double l3 = 0.0;
-        for (int k = tid; k < N; k += kTT) l3 = fma(r[k], z[k], l3);
+        for (int k = tid; k < N; k += kTT) l3 = fma(r[k], vs[k], l3);
         const double rz2 = tree_block_sum(l3, red);
         const double beta = rz2 / rz;
         rz = rz2;
-        for (int k = tid; k < N; k += kTT) p[k] = fma(beta, p[k], z[k]);
+        for (int k = tid; k < N; k += kTT) {           // p = z + beta p, kept in vs too
+            const double pk = fma(beta, p[k], vs[k]);
+            p[k] = pk;
+            vs[k] = pk;
+        }
+        __syncthreads();
     }
     __syncthreads();
     double l_s = 0.0, l_a = 0.0;

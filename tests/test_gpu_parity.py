@@ -288,7 +288,7 @@ def test_solve_full_size_reaches_exact_lp(P, name, outer_tol):
     gold = json.load(open(os.path.join(GOLD, f"exact_{name}.json")))
     w = make(name)
     pb = P.DeviceProblem.from_workload(w)
-    r = P.solve(pb, P.default_params(**dict(BENCH_A2, outer_tol=outer_tol)))
+    r = P.solve(pb, P.default_params(**dict(BENCH_A2, outer_tol=outer_tol, K=200000)))
     assert r["kkt"] <= 1e-8
     assert abs(r["obj"] - gold["obj"]) <= 1e-7 * abs(gold["obj"])
     assert r["status"] == 0

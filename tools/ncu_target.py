@@ -1,9 +1,10 @@
 """Short, deterministic targets for `ncu --set full` (one kernel family per mode).
 
-    python tools/ncu_target.py sweep|eval|cg [config]
+    python tools/ncu_target.py sweep|eval|cg|late [config]
 sweep: 30 Sinkhorn sweeps from X^0 (lse_pass_kernel); eval: 10 evaluations with
-sparsify (sum_pass_kernel); cg: a PINS solve capped at 10 outer iterations
-(cg_schur_cluster_kernel from the 6th on).  Inputs: the seeded workload.
+sparsify (sum_pass_kernel); cg: a PINS solve capped at 10 outer iterations;
+late: a PINS solve capped at 300 outer iterations (late-phase tree-PCG calls).
+Inputs: the seeded workload.
 """
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -26,6 +27,7 @@ if mode in ("sweep", "eval"):
         for _ in range(10):
             pins.evaluate(ws, pb, phi, psi, s, f, g, tau=1e-4 / (w.m * w.n))
 else:
-    r = pins.solve(pb, pins.default_params(K=10, outer_tol=0.0, newton_tol=1e-8))
+    K = 10 if mode == "cg" else 300
+    r = pins.solve(pb, pins.default_params(K=K, outer_tol=0.0, newton_tol=1e-8))
 torch.cuda.synchronize()
 print("ok", mode, name)
