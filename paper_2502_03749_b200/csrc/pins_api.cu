@@ -820,8 +820,10 @@ int run_eval(pins_workspace *ws, const pins_problem *pb, const double *phi, cons
                       ptr<long long>(ws->sb[0].blkoff)};
             CsrOut O1{ptr<long long>(ws->colptr), ptr<int>(ws->rowidx), ptr<double>(ws->valT),
                       ptr<long long>(ws->sb[1].blkoff)};
+            // long rows (early EPPA): warp per row, one lane per split segment
+            const int warpcopy = (double)nnz > 8.0 * (double)std::min(pb->m, pb->n) ? 1 : 0;
             LAUNCH(PINS_PROF_CSR, st, csr_build_kernel<<<A.side[0].RB + A.side[1].RB, kPT, 0, st>>>(
-                A.side[0], A.side[1], 2, O0, O1));
+                A.side[0], A.side[1], 2, O0, O1, warpcopy));
             PINS_CUDA(cudaGetLastError());
             ws->nnz = nnz;
             ws->csr_ready = ws->csc_ready = true;
@@ -868,7 +870,7 @@ int cg_blocks(pins_workspace *ws, long long N) {
 int run_cg(pins_workspace *ws, long long m, long long n, const long long *rowptr,
            const int *colidx, const double *val, const double *dr, const double *dc, double mu,
            const double *rhs, double *x, double rtol, int maxit, const double *gradf,
-           const double *gradg, const double *a, const double *b, cudaStream_t st) {
+           const double *gradg, const double *a, const double *b, cudaStream_t st, long long nnz_hint = -1) {
     const long long N = m + n;
     PINS_TRY(ensure(ws->cgvec, sizeof(double) * 4 * N));
     const int G = cg_blocks(ws, N);
@@ -901,6 +903,7 @@ int run_cg(pins_workspace *ws, long long m, long long n, const long long *rowptr
     A.a = a;
     A.b = b;
     A.st = ptr<double>(ws->cgst);
+    A.vec = (double)(nnz_hint >= 0 ? nnz_hint : ws->nnz) > 8.0 * (double)N ? 1 : 0;
     void *args[] = {&A};
     cudaError_t e_cg = cudaSuccess;
     LAUNCH(PINS_PROF_CG, st, e_cg = cudaLaunchCooperativeKernel((void *)cg_kernel, dim3(G), dim3(kThreads), args, 0, st));
@@ -1151,8 +1154,9 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
         acc[7] += hs[11];
         ++calls;
         if (calls % 200 == 1 || getenv("PINS_TREE_STATS")[0] == '2')
-            fprintf(stderr, "  last call: its %.0f rebuilt %.0f | kcycles mst %.1f fac %.1f pc %.1f mv %.1f total %.1f\n",
-                    cg_its, hs[11], hs[6] / 1e3, hs[7] / 1e3, hs[8] / 1e3, hs[9] / 1e3, hs[10] / 1e3);
+            fprintf(stderr, "  last call: its %.0f rebuilt %.0f | kcycles mst %.1f fac %.1f pc %.1f (fwd %.1f warp %.1f bwd %.1f, R0/RW %.0f) mv %.1f total %.1f\n",
+                    cg_its, hs[11], hs[6] / 1e3, hs[7] / 1e3, hs[8] / 1e3, hs[12] / 1e3, hs[13] / 1e3, hs[14] / 1e3,
+                    hs[15], hs[9] / 1e3, hs[10] / 1e3);
         if (calls % 200 == 1)
             fprintf(stderr, "tree-cg calls %ld nnz %lld its %.0f rebuilds %.0f | Mcycles mst %.1f fac %.1f pc %.1f mv %.1f total %.1f\n",
                     calls, ws->nnz, cg_its, acc[7], acc[2] / 1e6, acc[3] / 1e6, acc[4] / 1e6, acc[5] / 1e6, acc[6] / 1e6);
@@ -1322,7 +1326,7 @@ extern "C" int pins_cg(pins_workspace *ws, int64_t m, int64_t n, const int64_t *
     const long long *rp = reinterpret_cast<const long long *>(rowptr);
     PINS_TRY(build_csc(ws, m, n, rp, colidx, val, nnz, st));
     PINS_TRY(run_cg(ws, m, n, rp, colidx, val, dr, dc, mu, rhs, x, rtol, maxit, nullptr, nullptr,
-                    nullptr, nullptr, st));
+                    nullptr, nullptr, st, nnz));
     PINS_CUDA(cudaMemcpyAsync(ws->h + 16, ws->cgst.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     PINS_CUDA(cudaStreamSynchronize(st));
     *iters_host = (int32_t)ws->h[16];

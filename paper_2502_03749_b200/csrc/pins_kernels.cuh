@@ -499,6 +499,7 @@ struct CGArgs {
     int maxit;
     const double *gradf, *gradg, *a, *b;   // optional: slope / a.d terms
     double *st;
+    int vec;                               // 1: warp-per-row products (mean degree > 8)
 };
 
 __device__ __forceinline__ double block_sum(double v, double *sh) {
@@ -570,6 +571,30 @@ __global__ void __launch_bounds__(kThreads) cg_kernel(CGArgs A) {
         if (relres <= A.rtol || it >= A.maxit) break;
         // (A) w = M z ; q = w + beta q ; p = z + beta p ; <p,q>
         double l_pq = 0.0;
+        if (A.vec) {                       // dense-ish rows: one warp per row, lanes over entries
+            const int lane = threadIdx.x & 31;
+            const long long gw = gt >> 5, nw = gs >> 5;
+            for (long long k = gw; k < N; k += nw) {
+                double wv = 0.0;
+                if (k < A.m) {
+                    for (long long e = A.rowptr[k] + lane; e < A.rowptr[k + 1]; e += 32)
+                        wv = fma(A.val[e], A.z[A.m + A.colidx[e]], wv);
+                } else {
+                    const long long jj = k - A.m;
+                    for (long long e = A.colptr[jj] + lane; e < A.colptr[jj + 1]; e += 32)
+                        wv = fma(A.valT[e], A.z[A.rowidx[e]], wv);
+                }
+                wv = warp_sum(wv);
+                if (lane == 0) {
+                    wv = fma(diag(k), A.z[k], wv);
+                    const double qv = fma(beta, A.q[k], wv);
+                    const double pv = fma(beta, A.p[k], A.z[k]);
+                    A.q[k] = qv;
+                    A.p[k] = pv;
+                    l_pq = fma(pv, qv, l_pq);
+                }
+            }
+        } else
         for (long long k = gt; k < N; k += gs) {
             double wv;
             if (k < A.m) {

@@ -925,7 +925,7 @@ struct CsrOut {
 };
 
 __global__ void __launch_bounds__(kPT) csr_build_kernel(PassSide P0, PassSide P1, int nsides, CsrOut O0,
-                                                        CsrOut O1) {
+                                                        CsrOut O1, int warpcopy) {
     __shared__ long long sc[kPT];
     const int side = (blockIdx.x < (unsigned)P0.RB) ? 0 : 1;
     if (side == 1 && nsides < 2) return;
@@ -948,25 +948,55 @@ __global__ void __launch_bounds__(kPT) csr_build_kernel(PassSide P0, PassSide P1
         __syncthreads();
     }
     const long long start = O.blkoff[rb] + sc[tid] - tot;
-    if (i < P.M) {
-        O.ptr[i] = start;
-        long long dst = start;
-        for (int s0 = 0; s0 < P.S; s0 += 8) {          // counts of 8 splits in flight
-            int len[8];
+    __shared__ long long rstart_s[kPT];
+    rstart_s[tid] = start;
+    if (i < P.M && i == P.M - 1) O.ptr[P.M] = start + tot;
+    if (i < P.M) O.ptr[i] = start;
+    if (!warpcopy) {                                   // short rows: thread per row
+        if (i < P.M) {
+            long long dst = start;
+            for (int s0 = 0; s0 < P.S; s0 += 8) {
+                int len[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-                len[j] = s0 + j < P.S ? (int)min((long long)P.cnt[i * P.S + s0 + j], P.cap) : 0;
+                for (int j = 0; j < 8; ++j)
+                    len[j] = s0 + j < P.S ? (int)min((long long)P.cnt[i * P.S + s0 + j], P.cap) : 0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const long long src = (i * P.S + s0 + j) * P.cap;
-                for (int k = 0; k < len[j]; ++k) {
-                    O.idx[dst + k] = P.bcol[src + k];
-                    O.val[dst + k] = P.bval[src + k];
+                for (int j = 0; j < 8; ++j) {
+                    const long long src = (i * P.S + s0 + j) * P.cap;
+                    for (int k = 0; k < len[j]; ++k) {
+                        O.idx[dst + k] = P.bcol[src + k];
+                        O.val[dst + k] = P.bval[src + k];
+                    }
+                    dst += len[j];
                 }
-                dst += len[j];
             }
         }
-        if (i == P.M - 1) O.ptr[P.M] = dst;
+        return;
+    }
+    __syncthreads();
+    // copy: one warp per row, lane = split segment (exclusive scan of the segment
+    // lengths across the lanes gives each segment's offset inside the row)
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int rr = warp; rr < kPT; rr += kPT / 32) {
+        const long long ii = (long long)rb * kPT + rr;
+        if (ii >= P.M) break;
+        long long dst = rstart_s[rr];
+        for (int s0 = 0; s0 < P.S; s0 += 32) {
+            const int s = s0 + lane;
+            const int len = s < P.S ? (int)min((long long)P.cnt[ii * P.S + s], P.cap) : 0;
+            int x = len;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += t;
+            }
+            const long long my = dst + x - len;
+            const long long src = (ii * P.S + s) * P.cap;
+            for (int k = 0; k < len; ++k) {
+                O.idx[my + k] = P.bcol[src + k];
+                O.val[my + k] = P.bval[src + k];
+            }
+            dst += __shfl_sync(0xffffffffu, x, 31);
+        }
     }
 }
 

@@ -102,6 +102,20 @@ __device__ __forceinline__ double tree_block_sum(double v, double *sh) {
     return sh[32];
 }
 
+// packed factor record of one eliminated node (forward: y_v -= c * y_u; backward:
+// x_u = y_u inv - c1 x_v1 - c2 x_v2)
+struct Rec { int u, v1, v2, pad; double c1, c2, inv; };
+__device__ __forceinline__ Rec ldg_rec(const Rec *p) {
+    Rec r;
+    const int2 h0 = __ldg(reinterpret_cast<const int2 *>(p));        // 40-byte records: 8-byte aligned
+    const int2 h1 = __ldg(reinterpret_cast<const int2 *>(p) + 1);
+    r.u = h0.x; r.v1 = h0.y; r.v2 = h1.x; r.pad = 0;
+    r.c1 = __ldg(&p->c1);
+    r.c2 = __ldg(&p->c2);
+    r.inv = __ldg(&p->inv);
+    return r;
+}
+
 // smem double atomic add (CAS loop; conflicts are rare: a node receives at most
 // one update per eliminated neighbour per round)
 __device__ __forceinline__ void sm_add(double *p, double v) { atomicAdd(p, v); }
@@ -404,7 +418,6 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
     double *vs = reinterpret_cast<double *>(dyn);                             // N doubles
     // factor records packed (one 40-byte load per eliminated node); the late
     // (small) rounds are latency-bound, so their records also go to shared memory
-    struct Rec { int u, v1, v2, pad; double c1, c2, inv; };
     Rec *frec = reinterpret_cast<Rec *>(A.frec);
     const int nrec = A.rstart[nrounds];
     for (int qq = tid; qq < nrec; qq += kTT) {
@@ -427,18 +440,31 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
     while (RW > R0 && A.rstart[RW] - A.rstart[RW - 1] <= 32) --RW;
     const int warp_id = tid >> 5, lane_id = tid & 31;
     // in place on vs: forward elimination then back substitution (vs: r -> z)
+    long long tpf = 0, tpw = 0, tpb = 0;
     auto precond_inplace = [&]() {
+        const long long c0 = clock64();
         for (int rr = 0; rr < RW; ++rr) {
             const int q0r = A.rstart[rr], q1 = A.rstart[rr + 1];
-            const Rec *src = rr < R0 ? frec : tail - tbase;
-            for (int q = q0r + tid; q < q1; q += kTT) {
-                const Rec rc = src[q];
-                const double yu = vs[rc.u];
-                if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
-                if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+            if (rr < R0) {                        // read-only path: loads may run ahead
+#pragma unroll 2
+                for (int q = q0r + tid; q < q1; q += kTT) {
+                    const Rec rc = ldg_rec(frec + q);
+                    const double yu = vs[rc.u];
+                    if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
+                    if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+                }
+            } else {
+                const Rec *src = tail - tbase;
+                for (int q = q0r + tid; q < q1; q += kTT) {
+                    const Rec rc = src[q];
+                    const double yu = vs[rc.u];
+                    if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
+                    if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+                }
             }
             __syncthreads();
         }
+        const long long c1 = clock64();
         if (warp_id == 0) {
             const Rec *src = tail - tbase;
             for (int rr = RW; rr < nrounds; ++rr) {
@@ -464,18 +490,34 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
             }
         }
         __syncthreads();
+        const long long c2 = clock64();
         for (int rr = RW - 1; rr >= 0; --rr) {
             const int q0r = A.rstart[rr], q1 = A.rstart[rr + 1];
-            const Rec *src = rr < R0 ? frec : tail - tbase;
-            for (int q = q0r + tid; q < q1; q += kTT) {
-                const Rec rc = src[q];
-                double xu = vs[rc.u] * rc.inv;
-                if (rc.v1 >= 0) xu = fma(-rc.c1, vs[rc.v1], xu);
-                if (rc.v2 >= 0) xu = fma(-rc.c2, vs[rc.v2], xu);
-                vs[rc.u] = xu;
+            if (rr < R0) {
+#pragma unroll 2
+                for (int q = q0r + tid; q < q1; q += kTT) {
+                    const Rec rc = ldg_rec(frec + q);
+                    double xu = vs[rc.u] * rc.inv;
+                    if (rc.v1 >= 0) xu = fma(-rc.c1, vs[rc.v1], xu);
+                    if (rc.v2 >= 0) xu = fma(-rc.c2, vs[rc.v2], xu);
+                    vs[rc.u] = xu;
+                }
+            } else {
+                const Rec *src = tail - tbase;
+                for (int q = q0r + tid; q < q1; q += kTT) {
+                    const Rec rc = src[q];
+                    double xu = vs[rc.u] * rc.inv;
+                    if (rc.v1 >= 0) xu = fma(-rc.c1, vs[rc.v1], xu);
+                    if (rc.v2 >= 0) xu = fma(-rc.c2, vs[rc.v2], xu);
+                    vs[rc.u] = xu;
+                }
             }
             __syncthreads();
         }
+        const long long c3 = clock64();
+        tpf += c1 - c0;
+        tpw += c2 - c1;
+        tpb += c3 - c2;
     };
     const long long *rp = A.rowptr, *cp = A.colptr;
     double *x = A.x, *r = A.r, *p = A.p, *q = A.q;
@@ -595,6 +637,10 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
         A.st[9] = (double)t_mv;
         A.st[10] = (double)(clock64() - t_start);
         A.st[11] = rebuilt ? 1.0 : 0.0;
+        A.st[12] = (double)tpf;
+        A.st[13] = (double)tpw;
+        A.st[14] = (double)tpb;
+        A.st[15] = (double)(R0 * 1000 + RW);
     }
 }
 
