@@ -156,7 +156,7 @@ def kernel_roofline(cls: str, w, launches: int, ms: float, clocks_mhz: float, pe
 def oracle_rates(w, budget_s: float, cg_per_newton: float):
     """Time the oracle's own operations, as they stand, on the FULL instance at
     the first subproblem (k = 0, X^0 = a b^T): one Sinkhorn sweep, one residual
-    evaluation, and one Newton direction with 20 and with 40 CG iterations (the
+    evaluation, and one Newton direction with 10 and with 60 CG iterations (the
     difference gives the per-CG-iteration cost), plus one line-search trial.
     Returns seconds per operation."""
     import numpy as np
@@ -178,16 +178,16 @@ def oracle_rates(w, budget_s: float, cg_per_newton: float):
     out = dict(sweep=t_sweep, eval=t_eval, cost=t_cost)
     if spent + 6 * t_eval < budget_s:
         ts = []
-        for its in (20, 40):
+        for its in (10, 60):
             prm = po.Params(eta=w.eta, cg_tol=0.0, cg_forcing=0.0, cg_maxit=its)
             t0 = time.time()
             df, dg, _ = po.newton_direction(f, g, Ck, w.a, w.b, w.eta, prm)
             ts.append(time.time() - t0)
-        per_it = max(0.0, (ts[1] - ts[0]) / 20.0)
+        per_it = max(0.0, (ts[1] - ts[0]) / 50.0)
         t0 = time.time()
         po.dual_increase(f, g, df, dg, 1.0, Ck, w.a, w.b, w.eta)
         t_ls = time.time() - t0
-        out["newton"] = max(0.0, ts[0] - 20 * per_it) + per_it * cg_per_newton + t_ls
+        out["newton"] = max(0.0, ts[0] - 10 * per_it) + per_it * cg_per_newton + t_ls
         out["cg_it"] = per_it
     else:
         out["newton"] = 4 * t_eval      # plan + sparsify + one line-search trial, lower bound

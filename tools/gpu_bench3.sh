@@ -18,3 +18,4 @@ timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none -c 30000 
 python tools/summarize_launches.py /tmp/launches.csv gpurun_out/launches_r1b.json > /dev/null 2>&1
 gzip -c /tmp/launches.csv > gpurun_out/launches_r1b.csv.gz
 du -sh gpurun_out > gpurun_out/sizes.txt
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc $?" >> gpurun_out/smoke.log
