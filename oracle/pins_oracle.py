@@ -197,7 +197,7 @@ class Params:
     armijo_c: float = 1e-4        # reading R4
     beta: float = 0.5
     max_backtracks: int = 30
-    warm_start: int = 1           # reading R7: 1 carry (f,g) across outer iterations
+    warm_start: int = 1           # reading R7: 1 carry (f,g), 2 extrapolate (safeguarded), 0 zero
 
 
 def residual_l1(f, g, Ck, a, b, eta) -> float:
@@ -338,12 +338,23 @@ def pins(C: np.ndarray, a: np.ndarray, b: np.ndarray, prm: Params, trace: bool =
     tr: List[Dict] = []
     k = 0
     Ck = shifted_cost(C, logX, eta)
+    f_prev = g_prev = None
     for k in range(prm.K):
         Ck = shifted_cost(C, logX, eta)
         if not prm.warm_start:
             f = np.zeros(m)
             g = np.zeros(n)
+        # warm_start 2 (reading R7): linear extrapolation 2 x^k - x^{k-1} of the last two
+        # subproblem solutions, kept only if it needs no Sinkhorn phase
+        f_sol, g_sol = f, g
+        if prm.warm_start == 2 and f_prev is not None:
+            f, g = 2.0 * f_sol - f_prev, 2.0 * g_sol - g_prev
         res = residual_l1(f, g, Ck, a, b, eta)
+        if prm.warm_start == 2 and f_prev is not None and res > prm.sink_tol:
+            f, g = f_sol, g_sol
+            res = residual_l1(f, g, Ck, a, b, eta)
+        if k >= 1:
+            f_prev, g_prev = f_sol, g_sol
         t = 0
         while res > prm.sink_tol and t < prm.T1:
             f, g = sinkhorn_sweep(f, g, Ck, a, b, eta)

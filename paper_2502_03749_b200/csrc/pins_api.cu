@@ -153,6 +153,7 @@ struct pins_workspace {
     DevBuf rowptr, colidx, val, colcnt, colptr, cursor, rowidx, valT;
     DevBuf cgvec, cgpart, cgst, st, ft, gt, eu, ev, bu, bv, dir, rhs, tab, fsave, gsave, uv;
     DevBuf tr_i, tr_d, tr_u8, tr_u64;   // tree-CG workspace (int / double / byte / u64 pools)
+    DevBuf xprev, xsave;                // warm_start 2: previous solution, saved start
     // v2 dense passes
     SideBufs sb[2];
     DevBuf x32, y32, x64, y64, nx32, ny32, xh, yh, pinfo, ctl, gticket, pst, tol;
@@ -218,7 +219,7 @@ extern "C" void pins_workspace_destroy(pins_workspace *ws) {
                       &ws->dir, &ws->rhs, &ws->tab, &ws->fsave, &ws->gsave, &ws->uv, &ws->bu, &ws->bv,
                       &ws->x32, &ws->y32, &ws->x64, &ws->y64, &ws->nx32, &ws->ny32, &ws->xh, &ws->yh, &ws->pinfo,
                       &ws->ctl, &ws->gticket, &ws->pst, &ws->tol,
-                      &ws->tr_i, &ws->tr_d, &ws->tr_u8, &ws->tr_u64};
+                      &ws->tr_i, &ws->tr_d, &ws->tr_u8, &ws->tr_u64, &ws->xprev, &ws->xsave};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     for (int q = 0; q < 2; ++q) {
@@ -1434,7 +1435,28 @@ static int solve_core(const pins_problem *pb, const pins_params *prm, pins_resul
             PINS_CUDA(cudaMemsetAsync(f, 0, sizeof(double) * m, st));
             PINS_CUDA(cudaMemsetAsync(g, 0, sizeof(double) * n, st));
         }
+        // warm_start 2 (reading R7): start from the linear extrapolation of the last two
+        // subproblem solutions; fall back to the plain warm start if that would need Sinkhorn
+        const bool extrap = prm->warm_start == 2 && k >= 2;
+        if (prm->warm_start == 2) {
+            PINS_TRY(ensure(ws->xprev, sizeof(double) * (m + n)));
+            PINS_TRY(ensure(ws->xsave, sizeof(double) * (m + n)));
+            double *xp = ptr<double>(ws->xprev), *xs = ptr<double>(ws->xsave);
+            if (k == 1) {
+                PINS_CUDA(cudaMemcpyAsync(xp, f, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+                PINS_CUDA(cudaMemcpyAsync(xp + m, g, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+            } else if (extrap) {
+                LAUNCH(PINS_PROF_VEC, st, extrapolate_kernel<<<grid_1d(m, ws->nsm), 256, 0, st>>>(m, 1.0, 0, f, xp, xs));
+                LAUNCH(PINS_PROF_VEC, st, extrapolate_kernel<<<grid_1d(n, ws->nsm), 256, 0, st>>>(n, 1.0, 0, g, xp + m, xs + m));
+            }
+        }
         PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &cur));
+        if (extrap && !(cur.gnorm <= prm->sink_tol)) {
+            double *xp = ptr<double>(ws->xprev), *xs = ptr<double>(ws->xsave);
+            LAUNCH(PINS_PROF_VEC, st, extrapolate_kernel<<<grid_1d(m, ws->nsm), 256, 0, st>>>(m, 1.0, 1, f, xp, xs));
+            LAUNCH(PINS_PROF_VEC, st, extrapolate_kernel<<<grid_1d(n, ws->nsm), 256, 0, st>>>(n, 1.0, 1, g, xp + m, xs + m));
+            PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &cur));
+        }
         int t = 0;
         if (!(cur.gnorm <= prm->sink_tol) && prm->T1 > 0) {
             PINS_TRY(sinkhorn_phase(ws, pb, prm, phi, psi, s, f, g, cur.gnorm, &t, st));

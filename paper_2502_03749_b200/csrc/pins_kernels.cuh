@@ -717,6 +717,23 @@ __global__ void center_init_kernel(long long m, long long n, double eta, const d
     }
 }
 
+// warm start by linear extrapolation (warm_start = 2): x_prev <- x, x <- x + gamma (x - x_prev);
+// with undo = 1 restores x <- x_prev (the saved value)
+__global__ void extrapolate_kernel(long long len, double gamma, int undo, double *x, double *xprev,
+                                   double *xsave) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < len;
+         k += (long long)gridDim.x * blockDim.x) {
+        if (undo) {
+            x[k] = xsave[k];
+        } else {
+            const double cur = x[k];
+            xsave[k] = cur;
+            x[k] = fma(gamma, cur - xprev[k], cur);
+            xprev[k] = cur;
+        }
+    }
+}
+
 __global__ void center_update_kernel(long long m, long long n, double eta, const double *f,
                                      const double *g, double *phi, double *psi) {
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < m + n;

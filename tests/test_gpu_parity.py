@@ -253,13 +253,16 @@ def test_center_update_and_residuals(P):
     assert abs(rr["dual_inf"] - ko["dual_inf"]) <= 1e-12
 
 
-def test_solve_matches_oracle_fixed_iterations(P):
+@pytest.mark.parametrize("warm", [1, 2])
+def test_solve_matches_oracle_fixed_iterations(P, warm):
+    # warm_start 1: carry (f, g); 2: safeguarded linear extrapolation (reading R7)
     w = make("c1_rand1k", scale=0.1)
     C = po.cost_matrix(w)
     K = 25
-    o = po.pins(C, w.a, w.b, po.Params(eta=w.eta, K=K, outer_tol=0.0, newton_tol=1e-11), trace=True)
+    o = po.pins(C, w.a, w.b, po.Params(eta=w.eta, K=K, outer_tol=0.0, newton_tol=1e-11, warm_start=warm),
+                trace=True)
     pb = P.DeviceProblem.from_workload(w)
-    prm = P.default_params(K=K, outer_tol=0.0, newton_tol=1e-11)
+    prm = P.default_params(K=K, outer_tol=0.0, newton_tol=1e-11, warm_start=warm)
     r = P.solve(pb, prm, trace=True)
     assert r["outer_iters"] == K
     to = np.array([t["obj"] for t in o.trace])

@@ -251,3 +251,19 @@ def test_outer_rules():
     k_stop = next(k for k in range(2, 4000) if po.outer_converged(seq[:k], prm1))
     # error 1/k halves when k doubles: the halving estimate is exact for 1/k
     assert abs(1.0 / k_stop - 1e-3) < 2e-4
+
+
+@pytest.mark.parametrize("warm", [0, 1, 2])
+def test_pins_warm_start_variants_reach_exact_lp(warm):
+    # every warm-start reading (R7: zero, carry, safeguarded extrapolation) is only an
+    # initial point of subproblem (6); PINS must still reach the exact optimum of Eq. (1)
+    rng = np.random.default_rng(21)
+    m, n = 9, 7
+    C = rng.random((m, n))
+    a = rng.random(m) + 0.2; a /= a.sum()
+    b = rng.random(n) + 0.2; b /= b.sum()
+    ex = solve_exact(C, a, b)
+    r = po.pins(C, a, b, po.Params(eta=0.05, K=4000, outer_rule=1, outer_tol=1e-9, newton_tol=1e-11,
+                                    warm_start=warm))
+    assert abs(r.obj - ex["obj"]) <= 1e-7 * abs(ex["obj"])
+    assert r.kkt["primal"] <= 1e-9
