@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
     extern __shared__ __align__(16) unsigned char dyn[];   // 8 N bytes, reused by phase
     __shared__ double red[40];
     __shared__ int wsc[32];
+    __shared__ int rs[kTreeMaxRounds + 1];     // round boundaries (copy of A.rstart)
     __shared__ int s_flag, s_cnt;
     const int tid = threadIdx.x;
     const int m = A.m, n = A.n, N = m + n;
@@ -182,10 +183,11 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
             // numeric refactorisation on the stored schedule (push updates, round by round)
             nrounds = A.ctr[1];
             for (int v = tid; v < N; v += kTT) A.dcur[v] = (v < m ? A.dr[v] : A.dc[v - m]) + mu;
+            for (int k = tid; k <= nrounds; k += kTT) rs[k] = A.rstart[k];
             __syncthreads();
             for (int rr = 0; rr < nrounds; ++rr) {
-                const int q1 = A.rstart[rr + 1];
-                for (int q = A.rstart[rr] + tid; q < q1; q += kTT) {
+                const int q1 = rs[rr + 1];
+                for (int q = rs[rr] + tid; q < q1; q += kTT) {
                     const int s1 = A.fs1[q], s2 = A.fs2[q];
                     double w1 = 0.0, w2 = 0.0;
                     if (A.fv1[q] >= 0) {
@@ -436,15 +438,18 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
     __syncthreads();
     // the suffix of rounds with <= 32 records each is run by warp 0 alone, with
     // __syncwarp between rounds instead of a CTA barrier
+    // round boundaries in shared memory (read every round of every preconditioner apply)
+    for (int k = tid; k <= nrounds; k += kTT) rs[k] = A.rstart[k];
+    __syncthreads();
     int RW = nrounds;
-    while (RW > R0 && A.rstart[RW] - A.rstart[RW - 1] <= 32) --RW;
+    while (RW > R0 && rs[RW] - rs[RW - 1] <= 32) --RW;
     const int warp_id = tid >> 5, lane_id = tid & 31;
     // in place on vs: forward elimination then back substitution (vs: r -> z)
     long long tpf = 0, tpw = 0, tpb = 0;
     auto precond_inplace = [&]() {
         const long long c0 = clock64();
         for (int rr = 0; rr < RW; ++rr) {
-            const int q0r = A.rstart[rr], q1 = A.rstart[rr + 1];
+            const int q0r = rs[rr], q1 = rs[rr + 1];
             if (rr < R0) {                        // read-only path: loads may run ahead
 #pragma unroll 2
                 for (int q = q0r + tid; q < q1; q += kTT) {
@@ -468,8 +473,8 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
         if (warp_id == 0) {
             const Rec *src = tail - tbase;
             for (int rr = RW; rr < nrounds; ++rr) {
-                const int q = A.rstart[rr] + lane_id;
-                if (q < A.rstart[rr + 1]) {
+                const int q = rs[rr] + lane_id;
+                if (q < rs[rr + 1]) {
                     const Rec rc = src[q];
                     const double yu = vs[rc.u];
                     if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
@@ -478,8 +483,8 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
                 __syncwarp();
             }
             for (int rr = nrounds - 1; rr >= RW; --rr) {
-                const int q = A.rstart[rr] + lane_id;
-                if (q < A.rstart[rr + 1]) {
+                const int q = rs[rr] + lane_id;
+                if (q < rs[rr + 1]) {
                     const Rec rc = src[q];
                     double xu = vs[rc.u] * rc.inv;
                     if (rc.v1 >= 0) xu = fma(-rc.c1, vs[rc.v1], xu);
@@ -492,7 +497,7 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
         __syncthreads();
         const long long c2 = clock64();
         for (int rr = RW - 1; rr >= 0; --rr) {
-            const int q0r = A.rstart[rr], q1 = A.rstart[rr + 1];
+            const int q0r = rs[rr], q1 = rs[rr + 1];
             if (rr < R0) {
 #pragma unroll 2
                 for (int q = q0r + tid; q < q1; q += kTT) {
