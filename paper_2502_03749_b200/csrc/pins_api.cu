@@ -16,6 +16,7 @@
 #include "pins_cg.cuh"
 #include "pins_order.cuh"
 #include "pins_tree.cuh"
+#include "pins_treecl.cuh"
 
 using namespace pins;
 
@@ -168,6 +169,8 @@ struct pins_workspace {
     bool tree_valid = false;
     long long tree_N = -1;
     int tree_last_its = 0, tree_backoff = 0;
+    const int *tree_rstart = nullptr, *tree_ctr = nullptr;
+    const double *tree_frec = nullptr;
     bool csr_ready = false, csc_ready = false;
     double *h = nullptr;   // pinned host scalars (64)
 };
@@ -985,25 +988,24 @@ constexpr int kTreeMaxNodes = 26000;               // tree-solve vector in share
 constexpr long long kTreeNnzMax = 400000;
 bool use_tree_cg(pins_workspace *ws, long long m, long long n) {
     const char *e = getenv("PINS_CG");
-    if (e && strcmp(e, "tree") != 0) return false;
+    if (e && strcmp(e, "tree") != 0 && strcmp(e, "treecl") != 0) return false;
     // near-tree supports only (late EPPA: nnz ~ m + n, Thm 4.3); with many
     // off-tree edges the tree preconditioner loses its edge over Jacobi
     // adaptive: after a tree solve that needed many iterations (support far from
     // a tree), use the Jacobi-Schur cluster CG for a while, then try again
-    const bool forced = e && strcmp(e, "tree") == 0;
+    const bool forced = e && (strcmp(e, "tree") == 0 || strcmp(e, "treecl") == 0);
     if (!forced && ws->tree_backoff > 0) {
         --ws->tree_backoff;
         return false;
     }
-    // the tree preconditioner pays off when the support is close to a spanning tree
-    // (late EPPA iterations); far from it the Jacobi-Schur cluster CG is faster
-    const bool near_tree = (double)ws->nnz <= 1.25 * (double)(m + n);
-    return (forced || near_tree) && m + n <= kTreeMaxNodes && ws->nnz <= kTreeNnzMax && ws->csc_ready;
+    // tried by default; a solve that needs > 80 iterations (support far from a
+    // spanning tree) sends the next 256 Newton steps to the Jacobi-Schur cluster CG
+    return m + n <= kTreeMaxNodes && ws->nnz <= kTreeNnzMax && ws->csc_ready;
 }
 
 int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const double *rhs, double *x,
                 double rtol, int maxit, const double *gradf, const double *gradg, const double *a,
-                const double *b, cudaStream_t st) {
+                const double *b, cudaStream_t st, int setup_only = 0) {
     const long long N = m + n, nnz = std::max<long long>(ws->nnz, 1);
     PINS_TRY(ensure(ws->cgst, sizeof(double) * 16));
     // persistent arrays first, nnz-sized scratch last (offsets stay put as nnz changes)
@@ -1079,6 +1081,10 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     // reuse the stored tree while it keeps CG short (the kernel also checks that
     // every tree edge is still in the support and rebuilds otherwise)
     A.reuse = ws->tree_valid && ws->tree_last_its <= 48 ? 1 : 0;
+    A.setup_only = setup_only;
+    ws->tree_rstart = A.rstart;
+    ws->tree_ctr = A.ctr;
+    ws->tree_frec = A.frec;
     const size_t base = sizeof(double) * (size_t)N;
     const size_t budget = 220 * 1024;
     A.tail_cap = base < budget ? (int)((budget - base) / 40) : 0;
@@ -1093,6 +1099,55 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     PINS_CUDA(cudaGetLastError());
     ws->tree_valid = true;
     ws->tree_N = N;
+    return PINS_OK;
+}
+
+// Tree factor by the single-CTA kernel (setup only), then the PCG on one cluster:
+// CTAs 1..7 hold the vectors, CTA 0 applies the tree preconditioner (pins_treecl.cuh)
+int run_cg_tree_cluster(pins_workspace *ws, long long m, long long n, double mu, const double *rhs, double *x,
+                        double rtol, int maxit, const double *gradf, const double *gradg, const double *a,
+                        const double *b, cudaStream_t st) {
+    PINS_TRY(run_cg_tree(ws, m, n, mu, rhs, x, rtol, maxit, gradf, gradg, a, b, st, 1));
+    const long long N = m + n;
+    TreeCLArgs A;
+    memset(&A, 0, sizeof A);
+    A.m = (int)m;
+    A.n = (int)n;
+    A.rowptr = ptr<long long>(ws->rowptr);
+    A.colidx = ptr<int>(ws->colidx);
+    A.val = ptr<double>(ws->val);
+    A.colptr = ptr<long long>(ws->colptr);
+    A.rowidx = ptr<int>(ws->rowidx);
+    A.valT = ptr<double>(ws->valT);
+    A.dr = ptr<double>(ws->rowsum);
+    A.dc = ptr<double>(ws->colsum);
+    A.mu = mu;
+    A.rhs = rhs;
+    A.x = x;
+    A.rtol = rtol;
+    A.maxit = maxit;
+    A.gradf = gradf;
+    A.gradg = gradg;
+    A.a = a;
+    A.b = b;
+    A.st = ptr<double>(ws->cgst);
+    // the packed factor written by the setup kernel (pointers recorded by run_cg_tree)
+    A.rstart = ws->tree_rstart;
+    A.ctr = ws->tree_ctr;
+    A.frec = ws->tree_frec;
+    A.R = (int)((N + kTCW - 1) / kTCW);
+    const size_t base = sizeof(double) * (size_t)N;
+    const size_t budget = 220 * 1024;
+    A.tail_cap = base < budget ? (int)((budget - base) / 40) : 0;
+    const size_t smem = std::max<size_t>(base + (size_t)A.tail_cap * 40, sizeof(double) * 5 * (size_t)A.R);
+    static size_t configured = 0;
+    if (smem > configured) {
+        PINS_CUDA(cudaFuncSetAttribute(cg_tree_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<size_t>(smem, 48 * 1024)));
+        configured = std::max<size_t>(smem, 48 * 1024);
+    }
+    LAUNCH(PINS_PROF_CG, st, cg_tree_cluster_kernel<<<kCGC, kCGT, smem, st>>>(A));
+    PINS_CUDA(cudaGetLastError());
     return PINS_OK;
 }
 
@@ -1125,7 +1180,14 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
     const double rtol = cg_rtol(prm, cur->gnorm);
     double *d = ptr<double>(ws->dir);
     const bool used_tree = use_tree_cg(ws, m, n);
-    if (used_tree) {
+    const char *cgsel = getenv("PINS_CG");
+    // default tree path: factor on one CTA, PCG on a cluster; PINS_CG=tree keeps the
+    // whole PCG on the single CTA
+    const bool treecl = used_tree && !(cgsel && strcmp(cgsel, "tree") == 0);
+    if (treecl) {
+        PINS_TRY(run_cg_tree_cluster(ws, m, n, mu, rhs, d, rtol, prm->cg_maxit, ptr<double>(ws->gradf),
+                                     ptr<double>(ws->gradg), pb->a, pb->b, st));
+    } else if (used_tree) {
         PINS_TRY(run_cg_tree(ws, m, n, mu, rhs, d, rtol, prm->cg_maxit, ptr<double>(ws->gradf),
                              ptr<double>(ws->gradg), pb->a, pb->b, st));
     } else if (use_cluster_cg(ws, m, n) && !(getenv("PINS_CG") && strcmp(getenv("PINS_CG"), "cluster") != 0)) {

@@ -77,6 +77,7 @@ struct TreeArgs {
     int *fs1, *fs2;                    // [N] record slot sources
     double *fw1, *fw2;                 // [N] record slot weights
     int reuse;                         // 1: try the stored tree / schedule first
+    int setup_only;                    // 1: stop after the factor is packed (cluster PCG follows)
 };
 
 __device__ __forceinline__ unsigned hash_prio(unsigned u, unsigned r) {
@@ -427,6 +428,17 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
         rc.u = A.fu[qq]; rc.v1 = A.fv1[qq]; rc.v2 = A.fv2[qq]; rc.pad = 0;
         rc.c1 = A.fc1[qq]; rc.c2 = A.fc2[qq]; rc.inv = A.finv[qq];
         frec[qq] = rc;
+    }
+    if (A.setup_only) {
+        __syncthreads();
+        if (tid == 0) {
+            A.st[4] = (double)nrounds;
+            A.st[5] = (double)A.ctr[2];
+            A.st[6] = (double)t_mst;
+            A.st[7] = (double)t_fac;
+            A.st[11] = rebuilt ? 1.0 : 0.0;
+        }
+        return;
     }
     Rec *tail = reinterpret_cast<Rec *>(dyn + 8 * (size_t)N);
     const int tail_cap = A.tail_cap;

@@ -202,7 +202,7 @@ def test_cg_against_direct_solve(P):
     np.testing.assert_allclose(H(x), x_ref, rtol=1e-6, atol=1e-9 * np.abs(x_ref).max())
 
 
-@pytest.mark.parametrize("cg", ["tree", "cluster", "grid"])
+@pytest.mark.parametrize("cg", ["tree", "treecl", "cluster", "grid"])
 @pytest.mark.parametrize("name,mk", CASES[:5])
 def test_newton_step(P, name, mk, cg, monkeypatch):
     # the three Newton-system solvers: spanning-tree PCG (one CTA),
