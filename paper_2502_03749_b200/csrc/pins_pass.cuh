@@ -574,37 +574,20 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
                 for (int c = 0; c < kCC; ++c) dsc[c] = Dv[c];
             }
         }
-        // phase 2: the surviving entries of this row, in column order, two per step
-        // (two independent exponentials in flight; a new maximum takes the exact
-        // sequential update)
-        auto d_of = [&](int c) -> double {
-            if constexpr (COST == PC_SQTC) return (double)dsc[c];
-            else return chunk_dist<COST, DP>(B, P, rp, i, j0, c);
-        };
+        // phase 2: the surviving entries of this row, in column order (one exp each)
         while (mask) {
-            const int c1 = __ffs(mask) - 1;
+            const int c = __ffs(mask) - 1;
             mask &= mask - 1u;
-            const bool two = mask != 0u;
-            const int c2 = two ? __ffs(mask) - 1 : c1;
-            if (two) mask &= mask - 1u;
-            const double x1 = fma(-w, d_of(c1), B.q[c1]);
-            const double x2 = fma(-w, d_of(c2), B.q[c2]);
-            const double e1 = pexp_lean(fmax(-745.0, fmin(0.0, x1 - mx)), thi, tlo);
-            const double e2 = pexp_lean(fmax(-745.0, fmin(0.0, x2 - mx)), thi, tlo);
-            if (!(x1 > mx) && !(x2 > mx)) {
-                sm += e1;
-                if (two) sm += e2;
-            } else {
-                for (int t = 0; t < (two ? 2 : 1); ++t) {
-                    const double x = t == 0 ? x1 : x2;
-                    const double d = x - mx;
-                    const double e = pexp_lean(fmax(-745.0, -fabs(d)), thi, tlo);
-                    const bool up = d > 0.0;
-                    sm = up ? fma(sm, e, 1.0) : sm + e;
-                    mx = up ? x : mx;
-                    jm = up ? (int)(j0 + (t == 0 ? c1 : c2)) : jm;
-                }
-            }
+            double D;
+            if constexpr (COST == PC_SQTC) D = (double)dsc[c];
+            else D = chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+            const double x = fma(-w, D, B.q[c]);
+            const double d = x - mx;
+            const double e = pexp_lean(fmax(-745.0, -fabs(d)), thi, tlo);
+            const bool up = d > 0.0;
+            sm = up ? fma(sm, e, 1.0) : sm + e;
+            mx = up ? x : mx;
+            jm = up ? (int)(j0 + c) : jm;
         }
     });
     if constexpr (COST == PC_SQTC) tc_teardown(tcs);
@@ -737,11 +720,14 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
                 for (int c = 0; c < kCC; ++c) dsc[c] = Dv[c];
             }
         }
-        auto d_of = [&](int c) -> double {
-            if constexpr (COST == PC_SQTC) return (double)dsc[c];
-            else return chunk_dist<COST, DP>(B, P, rp, i, j0, c);
-        };
-        auto take = [&](int c, double D, double z, double X) {
+        while (mask) {
+            const int c = __ffs(mask) - 1;
+            mask &= mask - 1u;
+            double D;
+            if constexpr (COST == PC_SQTC) D = (double)dsc[c];
+            else D = chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+            const double z = fma(-w, D, __dadd_rn(Pi, B.q[c]));
+            const double X = pexp_lean(fmin(709.0, fmax(-745.0, z)), thi, tlo);
             acc += X;
             mz = fmax(mz, z);
             if (P.want_cx) cx = fma(X, D, cx);
@@ -756,20 +742,6 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
                 }
                 ++cnt;
             }
-        };
-        while (mask) {                               // two survivors per step, column order
-            const int c1 = __ffs(mask) - 1;
-            mask &= mask - 1u;
-            const bool two = mask != 0u;
-            const int c2 = two ? __ffs(mask) - 1 : c1;
-            if (two) mask &= mask - 1u;
-            const double D1 = d_of(c1), D2 = d_of(c2);
-            const double z1 = fma(-w, D1, __dadd_rn(Pi, B.q[c1]));
-            const double z2 = fma(-w, D2, __dadd_rn(Pi, B.q[c2]));
-            const double X1 = pexp_lean(fmin(709.0, fmax(-745.0, z1)), thi, tlo);
-            const double X2 = pexp_lean(fmin(709.0, fmax(-745.0, z2)), thi, tlo);
-            take(c1, D1, z1, X1);
-            if (two) take(c2, D2, z2, X2);
         }
     });
     if constexpr (COST == PC_SQTC) tc_teardown(tcs);
