@@ -219,6 +219,24 @@ def blas_threads() -> int:
         return os.cpu_count() or 1
 
 
+# ------------------------------------------------------------------ multi-GPU
+def max_over_ranks(local: float, world: int, device: str) -> float:
+    """Device time of the job = the slowest rank's (timing rule: max over ranks)."""
+    if world <= 1:
+        return float(local)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(local)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def per_solve_value(total_s: float, steps: int, world: int) -> float:
+    """Whole-job seconds per solve: N replicas each solve `steps` independent problems
+    in total_s (max over ranks), so the job delivers steps * N solves in total_s."""
+    return total_s / (steps * world)
+
+
 # ------------------------------------------------------------------ main
 def run_reference(args, rank):
     if rank != 0:
@@ -308,11 +326,8 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     for r in results:
         check(r)
-    tot_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
-    T = tot_ms.item() / 1e3
-    value = T / (args.steps * world)
+    T = max_over_ranks(sum(step_ms), world, "cuda") / 1e3
+    value = per_solve_value(T, args.steps, world)
 
     # ---- end to end through the host-buffer C-ABI call ----
     hp = pins.HostProblem(w)
@@ -328,10 +343,8 @@ def main():
         check(r)
         io = (r["h2d_bytes"], r["d2h_bytes"])
     barrier()
-    e2e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in e2e_ev)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = e2e_ms.item() / 1e3 / (args.steps * world)
+    e2e_value = per_solve_value(max_over_ranks(sum(a.elapsed_time(b) for a, b in e2e_ev), world, "cuda") / 1e3,
+                                args.steps, world)
 
     if rank == 0:
         r0 = results[-1]

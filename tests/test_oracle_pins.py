@@ -267,3 +267,89 @@ def test_pins_warm_start_variants_reach_exact_lp(warm):
                                     warm_start=warm))
     assert abs(r.obj - ex["obj"]) <= 1e-7 * abs(ex["obj"])
     assert r.kkt["primal"] <= 1e-9
+
+
+# ------------------------------------------------------------------ remaining pins
+def test_cost_matrix_closed_form_and_scaling():
+    # input definition: squared-Euclidean / L1 distances of lattice points,
+    # scaled so that the largest entry is 1; 3-4-5 triangle gives D = 25 (sq) and 7 (L1)
+    from workloads.gen import _points_workload, COST_SQEUCLID, COST_L1
+    X = np.array([[0.0, 0.0], [3.0, 4.0]])
+    Y = np.array([[0.0, 0.0], [3.0, 0.0]])
+    a = b = np.array([0.5, 0.5])
+    w = _points_workload("t", X, Y, COST_SQEUCLID, a, b, 0.1)
+    C = po.cost_matrix(w)
+    np.testing.assert_allclose(C * 25.0, [[0.0, 9.0], [25.0, 16.0]], rtol=0, atol=1e-13)
+    w = _points_workload("t", X, Y, COST_L1, a, b, 0.1)
+    C = po.cost_matrix(w)
+    np.testing.assert_allclose(C * 7.0, [[0.0, 3.0], [7.0, 4.0]], rtol=0, atol=1e-13)
+    assert C.max() == 1.0
+
+
+def test_logsumexp_identities():
+    # log sum exp = log(sum(exp)) for moderate values; exact shift invariance for huge ones
+    rng = np.random.default_rng(3)
+    A = rng.normal(size=(5, 7))
+    np.testing.assert_allclose(po.logsumexp(A, 1), np.log(np.exp(A).sum(1)), rtol=1e-14)
+    np.testing.assert_allclose(po.logsumexp(A + 1000.0, 0), np.log(np.exp(A).sum(0)) + 1000.0, rtol=1e-14)
+    B = np.array([[-np.inf, 0.0], [-np.inf, -np.inf]])
+    with np.errstate(divide="ignore"):
+        L = po.logsumexp(B, 1)
+    assert L[0] == 0.0 and L[1] == -np.inf
+
+
+def test_cg_rtol_forcing_term():
+    # reading R5: clamp(cg_forcing * newton_tol / ||grad||_1, cg_tol, 0.5)
+    prm = po.Params(newton_tol=1e-8, cg_tol=1e-6, cg_forcing=0.1)
+    assert po.cg_rtol(1e-8, prm) == pytest.approx(0.1)
+    assert po.cg_rtol(1e-10, prm) == 0.5
+    assert po.cg_rtol(1.0, prm) == 1e-6
+    assert po.cg_rtol(1e-3, po.Params(cg_forcing=0.0, cg_tol=1e-9)) == 1e-9
+
+
+def test_dual_increase_matches_direct_difference():
+    # Eq. (8) rearranged (reading R4) equals P(x + alpha d) - P(x) where the direct
+    # difference is well conditioned
+    rng = np.random.default_rng(8)
+    m, n, eta = 4, 5, 0.3
+    Ck = rng.random((m, n))
+    a = po_norm(rng.random(m) + 0.1); b = po_norm(rng.random(n) + 0.1)
+    f, g = rng.normal(0, 0.2, m), rng.normal(0, 0.2, n)
+    df, dg = rng.normal(0, 0.1, m), rng.normal(0, 0.1, n)
+    for alpha in (1.0, 0.25):
+        direct = (po.dual_objective(f + alpha * df, g + alpha * dg, Ck, a, b, eta)
+                  - po.dual_objective(f, g, Ck, a, b, eta))
+        assert abs(po.dual_increase(f, g, df, dg, alpha, Ck, a, b, eta) - direct) <= 1e-14
+
+
+def test_line_search_returns_largest_armijo_step():
+    # backtracking (reading R4): the accepted alpha satisfies the
+    # Armijo condition and 2 alpha (if tried) does not
+    rng = np.random.default_rng(9)
+    m, n, eta = 6, 5, 0.05
+    Ck = rng.random((m, n))
+    a = po_norm(rng.random(m) + 0.1); b = po_norm(rng.random(n) + 0.1)
+    f, g = np.zeros(m), np.zeros(n)
+    prm = po.Params(eta=eta)
+    gf, gg = po.dual_gradient(f, g, Ck, a, b, eta)
+    df, dg = 40.0 * gf, 40.0 * gg            # an over-long ascent direction forces backtracking
+    alpha, inc = po.line_search(f, g, df, dg, Ck, a, b, eta, prm)
+    slope = float(gf @ df + gg @ dg)
+    assert 0.0 < alpha < 1.0
+    assert inc >= prm.armijo_c * alpha * slope
+    big = 2.0 * alpha
+    assert po.dual_increase(f, g, df, dg, big, Ck, a, b, eta) < prm.armijo_c * big * slope
+
+
+def test_kkt_of_exact_lp_solution():
+    # residuals of Eq. (1) at the network simplex optimum and its dual certificate:
+    # feasible plan, dual feasible up to rounding, zero duality gap
+    rng = np.random.default_rng(12)
+    m, n = 7, 9
+    C = rng.random((m, n))
+    a = po_norm(rng.random(m) + 0.1); b = po_norm(rng.random(n) + 0.1)
+    ex = solve_exact(C, a, b)
+    with np.errstate(divide="ignore"):
+        logX = np.log(ex["X"])
+    k = po.kkt(C, logX, a, b, ex["u"], ex["v"])
+    assert k["primal"] <= 1e-14 and k["dual_inf"] <= 1e-13 and abs(k["gap"]) <= 1e-13
