@@ -80,7 +80,9 @@ typedef struct pins_params {
     double armijo_c;         /* (1e-4) */
     double beta;             /* backtracking factor (0.5) */
     int32_t max_backtracks;  /* (30) */
-    int32_t warm_start;      /* 1 carry (f,g) across outer iterations      (1)    */
+    int32_t warm_start;      /* 0 zero, 1 carry (f,g) across outer iterations, 2 linear
+                                extrapolation 2x^k - x^{k-1} kept only if it needs no
+                                Sinkhorn phase (R7)               (1)    */
 } pins_params;
 
 void pins_default_params(pins_params *p);
@@ -185,7 +187,16 @@ typedef struct pins_result {
     double seconds;          /* host wall time of the solve                      */
 } pins_result;
 
-/* Full PINS solve, Algorithm 2.  Synchronises.            */
+/* Full PINS solve, Algorithm 2.  Synchronises.
+ * Point costs are solved on a copy permuted into Morton order of the
+ * coordinates (locality for the dense passes) and the potentials are scattered
+ * back, so every output is in the caller's order.  The Newton systems use the
+ * spanning-tree preconditioned CG when m + n <= 26000 and nnz <= 4e5 (falling
+ * back to the Jacobi-Schur cluster CG after a slow tree solve), else Jacobi CG
+ * on the whole GPU.  Development knobs (environment):
+ * PINS_CG = tree | treecl | cluster | grid forces a solver, PINS_NO_TC=1 turns
+ * the tensor-core cross term off, PINS_NO_REORDER=1 the Morton permutation,
+ * PINS_TRACE=<file> writes one line per outer iteration.                     */
 int pins_solve(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream);
 
 /* End-to-end solve from HOST memory (bench.py's e2e leg): pb_host is a
