@@ -158,10 +158,12 @@ struct pins_workspace {
     // v2 dense passes
     SideBufs sb[2];
     DevBuf x32, y32, x64, y64, nx32, ny32, xh, yh, pinfo, ctl, gticket, pst, tol;
+    DevBuf bx128, bx32, by128, by32;    // tile-skip boxes (row blocks / column groups)
+    DevBuf dmin0, dmin1, skst;          // Dmin tables per orientation, adaptive switch states
     const void *key_C = nullptr, *key_x = nullptr, *key_y = nullptr;
     long long key_m = -1, key_n = -1, key_ldc = -1;
     int key_kind = -1, key_d = -1;
-    int cost_row = 0, cost_col = 0, dp = 4;
+    int cost_row = 0, cost_col = 0, dp = 4, skipk = 0;
     int S[2] = {1, 1};
     long long pcap = 16;       // per (row, split) sparsify capacity
     long long m = 0, n = 0, cap = 64, nnz = 0;
@@ -593,6 +595,34 @@ int prepare_pass(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
             exact32 = integral && 2.0 * pb->d * std::max(ax, ay) < two24;
             ws->cost_row = ws->cost_col = exact32 ? PC_L132 : PC_L164;
         }
+        // tile skipping needs exact fp32 distances (integer points, R10)
+        ws->skipk = 0;
+        if (exact32 && getenv("PINS_NO_TILESKIP") == nullptr) {
+            ws->skipk = pb->cost_kind == PINS_COST_SQEUCLID ? 1 : 2;
+            const long long gx128 = (m + kPT - 1) / kPT, gy128 = (n + kPT - 1) / kPT;
+            const long long gx32 = (m + kCC - 1) / kCC, gy32 = (n + kCC - 1) / kCC;
+            PINS_TRY(ensure(ws->bx128, sizeof(float) * gx128 * 2 * dp));
+            PINS_TRY(ensure(ws->by128, sizeof(float) * gy128 * 2 * dp));
+            PINS_TRY(ensure(ws->bx32, sizeof(float) * gx32 * 2 * dp));
+            PINS_TRY(ensure(ws->by32, sizeof(float) * gy32 * 2 * dp));
+            LAUNCH(PINS_PROF_VEC, st, box_kernel<<<grid_1d(gx128 * dp, ws->nsm), 256, 0, st>>>(
+                m, dp, kPT, ptr<float>(ws->x32), ptr<float>(ws->bx128)));
+            LAUNCH(PINS_PROF_VEC, st, box_kernel<<<grid_1d(gy128 * dp, ws->nsm), 256, 0, st>>>(
+                n, dp, kPT, ptr<float>(ws->y32), ptr<float>(ws->by128)));
+            LAUNCH(PINS_PROF_VEC, st, box_kernel<<<grid_1d(gx32 * dp, ws->nsm), 256, 0, st>>>(
+                m, dp, kCC, ptr<float>(ws->x32), ptr<float>(ws->bx32)));
+            LAUNCH(PINS_PROF_VEC, st, box_kernel<<<grid_1d(gy32 * dp, ws->nsm), 256, 0, st>>>(
+                n, dp, kCC, ptr<float>(ws->y32), ptr<float>(ws->by32)));
+            PINS_TRY(ensure(ws->dmin0, sizeof(float) * gx128 * gy32));
+            PINS_TRY(ensure(ws->dmin1, sizeof(float) * gy128 * gx32));
+            LAUNCH(PINS_PROF_VEC, st, dmin_kernel<<<grid_1d(gx128 * gy32, ws->nsm), 256, 0, st>>>(
+                gx128, gy32, dp, ws->skipk, ptr<float>(ws->bx128), ptr<float>(ws->by32), ptr<float>(ws->dmin0)));
+            LAUNCH(PINS_PROF_VEC, st, dmin_kernel<<<grid_1d(gy128 * gx32, ws->nsm), 256, 0, st>>>(
+                gy128, gx32, dp, ws->skipk, ptr<float>(ws->by128), ptr<float>(ws->bx32), ptr<float>(ws->dmin1)));
+            PINS_TRY(ensure(ws->skst, sizeof(int) * 16));
+            PINS_CUDA(cudaMemsetAsync(ws->skst.p, 0, sizeof(int) * 16, st));
+            PINS_CUDA(cudaGetLastError());
+        }
     }
     ws->key_C = pb->C; ws->key_x = pb->x; ws->key_y = pb->y; ws->key_m = m; ws->key_n = n;
     ws->key_kind = pb->cost_kind; ws->key_d = pb->d; ws->key_ldc = pb->ldc;
@@ -619,6 +649,10 @@ void fill_side(pins_workspace *ws, const pins_problem *pb, int o, const double *
     P.yc64 = ptr<double>(row ? ws->y64 : ws->x64);
     P.xrh = ptr<__half>(row ? ws->xh : ws->yh);
     P.ych = ptr<__half>(row ? ws->yh : ws->xh);
+    P.skipk = pb->cost_kind == PINS_COST_DENSE ? 0 : ws->skipk;
+    P.dmin = ptr<float>(row ? ws->dmin0 : ws->dmin1);
+    P.ng = (P.N + kCC - 1) / kCC;
+    P.skst = ptr<int>(ws->skst) + 4 * (2 + o);     // sum passes; half_sweep uses states 0 / 1
     P.fr = row ? f : g;
     P.phir = row ? phi : psi;
     P.gc = row ? g : f;
@@ -698,6 +732,7 @@ int half_sweep(pins_workspace *ws, const pins_problem *pb, int o, const double *
     PassArgs A;
     base_args(ws, pb, s, A);
     fill_side(ws, pb, o, f, phi, g, psi, A.side[0]);
+    A.side[0].skst = ptr<int>(ws->skst) + 4 * o;
     A.side[0].fout = o == 0 ? f : g;
     A.side[0].fsave = o == 0 ? ptr<double>(ws->fsave) : nullptr;
     A.nsides = 1;

@@ -65,6 +65,12 @@ struct PassSide {
     const float *nxr, *nyc;         // squared norms (PC_SQ32)
     const double *xr64, *yc64;      // fp64 points, M x dp / N x dp (zero padded)
     const __half *xrh, *ych;        // PC_SQTC: fp16 points, M x 16 / N x 16 (zero padded)
+    // tile skipping (exact-fp32 point costs): bounding boxes [lo[dp], hi[dp]] of the
+    // pass rows per row block (kPT rows) and of the pass columns per group of kCC
+    int skipk;                      // 0 off, 1 squared Euclidean, 2 L1
+    const float *dmin;              // [RB x ceil(N / kCC)]: box distance lower bound (rounded down)
+    long long ng;                   // ceil(N / kCC)
+    int *skst;                      // adaptive switch: [0] passes left disabled, [1] skipped, [2] chunks
     // potentials: pass-row side (fr + phir), pass-column side (gc + psic)
     const double *fr, *phir, *gc, *psic;
     int m1_row;                     // SUM: the "-1" of Eq. (7) sits on the pass-row potential
@@ -140,6 +146,7 @@ struct Buf {
     double ev[kCC];                              // trial factor
     alignas(16) float qs[kCC];                   // fp32 skip-test value: qt rounded up by 2^-20 |qt|
     alignas(16) float ny[kCC];
+    int skip;                                    // whole chunk below every row's threshold
     alignas(16) float y32[PTS32 ? kCC * DP : 4];
     double y64[PTS64 ? kCC * DP : 1];
     alignas(128) unsigned char yh[COST == PC_SQTC ? kCC * 32 : 16];   // UMMA B tile (kCC x 16 fp16)
@@ -149,19 +156,33 @@ struct Buf {
 template <int COST>
 constexpr int kNBuf = COST == PC_DENSE_ROW ? 1 : 2;
 
+// Whole-chunk skip (R10, tile form).  With integer points every fp32 distance Df
+// is exact, so Df >= Dmin, the distance between the row block's box and the
+// chunk's box.  If  max_c qs_c - w_lo Dmin <= min_i thr32_i  then no entry of the
+// chunk passes the per-entry fp32 test (fl is monotone and thr32 representable),
+// so skipping the chunk changes nothing: results are bit-identical with and
+// without it.  thrmin is a lower bound of every row's thr32 over the whole pass.
+struct SkipCtx {
+    int kind;                   // 0: never skip
+    float thrmin, w_lo;
+    const float *drow;          // the row block's row of the Dmin table
+};
+
 template <int COST, int DP>
 struct Pref {
     static constexpr bool PTS32 = COST == PC_SQ32 || COST == PC_L132;
     static constexpr bool PTS64 = COST == PC_SQ64 || COST == PC_L164;
     static constexpr int NY = (PTS32 || PTS64) ? (kCC * DP + kPT - 1) / kPT : 1;
     double g, psi, ev, bv;
-    float ny;
+    float ny, dm;                                // owner warp lane 0: the chunk's Dmin
     float y32[PTS32 ? NY : 1];
     double y64[PTS64 ? NY : 1];
     uint2 yh;
     // global -> registers (this thread's share of columns j0 .. j0+nc-1)
-    __device__ __forceinline__ void load(const PassSide &P, long long j0, int nc, bool trial) {
+    __device__ __forceinline__ void load(const PassSide &P, long long j0, int nc, bool trial, const SkipCtx &sk) {
         const int tid = threadIdx.x;
+        if (sk.kind && tid == (trial ? kCC : 0) && nc > 0)
+            dm = fminf(__ldg(sk.drow + j0 / kCC), __ldg(sk.drow + (j0 + nc - 1) / kCC));
         if (tid < kCC) {
             const bool ok = tid < nc;
             g = ok ? P.gc[j0 + tid] : 0.0;
@@ -199,18 +220,33 @@ struct Pref {
             }
         }
     }
+    // owner warp: the chunk skip decision from this lane's qs value (all 32 lanes)
+    __device__ __forceinline__ void decide(Buf<COST, DP> &B, const SkipCtx &sk, float qs) const {
+        const int lane = threadIdx.x & 31;
+        float qm = qs;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+        if (lane == 0) {
+            const double wd = (double)sk.w_lo * (double)dm;
+            const double lhs = (double)qm - wd;
+            B.skip = lhs + 1e-14 * (fabs((double)qm) + wd) <= (double)sk.thrmin;
+        }
+    }
     // registers -> shared buffer.  qmode: 0 q = (g+psi)/eta, 1 q = (g+psi)/eta - 1
     __device__ __forceinline__ void store(Buf<COST, DP> &B, const PassSide &P, long long i0, long long j0, int nc,
-                                          double inv_eta, int qmode, bool trial) {
+                                          double inv_eta, int qmode, bool trial, const SkipCtx &sk) {
         const int tid = threadIdx.x;
         if (tid < kCC) {
             double q = -INFINITY;
             if (tid < nc) q = qmode ? pot_p(g, psi, inv_eta) : pot_q(g, psi, inv_eta);
             B.q[tid] = q;
             if (!trial) {
+                const float qs = qs_of(q);
                 B.qt[tid] = q;
-                B.qs[tid] = qs_of(q);
-            }
+                B.qs[tid] = qs;
+                if (sk.kind) decide(B, sk, qs);
+                else if (tid == 0) B.skip = 0;
+            } else if (tid == 0) B.skip = 0;
         } else if (tid < 2 * kCC && trial) {
             B.ev[tid - kCC] = ev;
         }
@@ -244,13 +280,15 @@ struct Pref {
         }
     }
     // trial: the skip-test value q + bv needs q, written by threads < kCC
-    __device__ __forceinline__ void store_trial_qt(Buf<COST, DP> &B) {
+    __device__ __forceinline__ void store_trial_qt(Buf<COST, DP> &B, const SkipCtx &sk) {
         const int tid = threadIdx.x;
         if (tid >= kCC && tid < 2 * kCC) {
             const int c = tid - kCC;
             const double qt = B.q[c] + bv;
+            const float qs = qs_of(qt);
             B.qt[c] = qt;
-            B.qs[c] = qs_of(qt);
+            B.qs[c] = qs;
+            if (sk.kind) decide(B, sk, qs);
         }
     }
 };
@@ -363,25 +401,29 @@ using TcFor = typename std::conditional<COST == PC_SQTC, TcState, TcStateT<16>>:
 // body(c0, nc, buf, dots) per chunk: for PC_SQTC `dots` holds this thread's
 // kCC dot products x_i.y_j from TMEM; for the other costs it is unused.
 template <int COST, int DP, class TS, class Body>
-__device__ __forceinline__ void stream_columns(const PassSide &P, long long i0, long long jb, long long je,
-                                               double inv_eta, int qmode, bool trial, Buf<COST, DP> *bufs,
-                                               TS *tcs, Body body) {
+__device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, long long jb, long long je,
+                                              double inv_eta, int qmode, bool trial, Buf<COST, DP> *bufs,
+                                              TS *tcs, const SkipCtx &sk, Body body) {
     constexpr int NB = kNBuf<COST>;
     const long long nch = (je - jb + kCC - 1) / kCC;
-    if (nch <= 0) return;
+    if (nch <= 0) return 0;
+    int nskip = 0;
     const int tid = threadIdx.x, warp = tid >> 5;
     Pref<COST, DP> pf;
     constexpr uint32_t idesc = tc::make_idesc(kCC);
     auto nc_of = [&](long long c) { return (int)min((long long)kCC, je - (jb + c * kCC)); };
+    // MMAs are issued only for chunks that are not skipped; the parity of each
+    // buffer's mbarrier advances once per issued MMA
+    uint32_t par = 0u;                               // bit b: parity of buffer b's next phase
     // prologue: chunk 0 into buffer 0, prefetch chunk 1
-    pf.load(P, jb, nc_of(0), trial);
-    pf.store(bufs[0], P, i0, jb, nc_of(0), inv_eta, qmode, trial);
-    if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0]); }
-    if (NB > 1 && nch > 1) pf.load(P, jb + kCC, nc_of(1), trial);
+    pf.load(P, jb, nc_of(0), trial, sk);
+    pf.store(bufs[0], P, i0, jb, nc_of(0), inv_eta, qmode, trial, sk);
+    if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0], sk); }
+    if (NB > 1 && nch > 1) pf.load(P, jb + kCC, nc_of(1), trial, sk);
     if constexpr (COST == PC_SQTC) tc::fence_proxy_async();
     __syncthreads();
     if constexpr (COST == PC_SQTC) {
-        if (tid == 0) {
+        if (tid == 0 && !bufs[0].skip) {
             tc::fence_after();
             tc::mma_f16(tcs->tbase, tc::make_desc(tcs->ah), tc::make_desc(bufs[0].yh), idesc);
             tc::commit(&tcs->mbar[0]);
@@ -393,13 +435,13 @@ __device__ __forceinline__ void stream_columns(const PassSide &P, long long i0, 
             const int nxt = cur ^ 1;
             if constexpr (COST == PC_SQTC) tc::fence_before();
             __syncthreads();                         // chunk c-1 fully consumed
-            pf.store(bufs[nxt], P, i0, jb + (c + 1) * kCC, nc_of(c + 1), inv_eta, qmode, trial);
-            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[nxt]); }
-            if (c + 2 < nch) pf.load(P, jb + (c + 2) * kCC, nc_of(c + 2), trial);
+            pf.store(bufs[nxt], P, i0, jb + (c + 1) * kCC, nc_of(c + 1), inv_eta, qmode, trial, sk);
+            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[nxt], sk); }
+            if (c + 2 < nch) pf.load(P, jb + (c + 2) * kCC, nc_of(c + 2), trial, sk);
             if constexpr (COST == PC_SQTC) tc::fence_proxy_async();
             __syncthreads();
             if constexpr (COST == PC_SQTC) {
-                if (tid == 0) {
+                if (tid == 0 && !bufs[nxt].skip) {
                     tc::fence_after();
                     tc::mma_f16(tcs->tbase + nxt * kCC, tc::make_desc(tcs->ah), tc::make_desc(bufs[nxt].yh), idesc);
                     tc::commit(&tcs->mbar[nxt]);
@@ -407,19 +449,40 @@ __device__ __forceinline__ void stream_columns(const PassSide &P, long long i0, 
             }
         } else if (NB == 1 && c > 0) {
             __syncthreads();
-            pf.load(P, jb + c * kCC, nc_of(c), trial);
-            pf.store(bufs[0], P, i0, jb + c * kCC, nc_of(c), inv_eta, qmode, trial);
-            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0]); }
+            pf.load(P, jb + c * kCC, nc_of(c), trial, sk);
+            pf.store(bufs[0], P, i0, jb + c * kCC, nc_of(c), inv_eta, qmode, trial, sk);
+            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0], sk); }
             __syncthreads();
         }
+        if (bufs[cur].skip) { ++nskip; continue; }   // read before the next chunk boundary's barrier
         float dots[COST == PC_SQTC ? kCC : 1];
         if constexpr (COST == PC_SQTC) {
-            tc::mbar_wait(&tcs->mbar[cur], (uint32_t)((c >> 1) & 1));
+            tc::mbar_wait(&tcs->mbar[cur], (par >> cur) & 1u);
+            par ^= 1u << cur;
             tc::fence_after();
             tc::ld32(tcs->tbase + ((uint32_t)(32 * (warp & 3)) << 16) + cur * kCC, dots);
         }
         body(jb + c * kCC, nc_of(c), bufs[cur], dots);
     }
+    return nskip;
+}
+
+// skip statistics of one CTA (thread 0), and the launch finalizer's switch: a pass
+// that skipped < 5 % of its chunks turns skipping off for the next 16 passes
+__device__ __forceinline__ void skip_count(const PassSide &P, const SkipCtx &sk, int nskip, long long jb,
+                                           long long je) {
+    if (threadIdx.x == 0 && sk.kind) {
+        atomicAdd(P.skst + 1, nskip);
+        atomicAdd(P.skst + 2, (int)((je - jb + kCC - 1) / kCC));
+    }
+}
+__device__ __forceinline__ void skip_switch(const PassSide &P) {
+    if (!P.skipk) return;
+    int *s = P.skst;
+    if (s[0] > 0) { s[0] -= 1; return; }
+    s[0] = (20LL * s[1] < (long long)s[2]) ? 16 : 0;
+    s[1] = 0;
+    s[2] = 0;
 }
 
 // CTA-level tensor-core setup / teardown (PC_SQTC only)
@@ -501,6 +564,27 @@ __device__ __forceinline__ double block_reduce_max(double v, double *sh) {
     return t;
 }
 
+// CTA setup of the chunk skip: the minimum over the CTA's valid rows of the fp32 threshold (block-wide; contains
+// __syncthreads, call from all threads).
+template <int DP>
+__device__ __forceinline__ SkipCtx skip_setup(const PassSide &P, int rb, bool valid, float thr32, float w_lo,
+                                              float *red32) {
+    SkipCtx sk{0, -INFINITY, w_lo, P.dmin + (long long)rb * P.ng};
+    if (!P.skipk || P.skst[0] > 0) return sk;     // off, or switched off for this pass
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    float t = valid ? thr32 : INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = fminf(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (lane == 0) red32[warp] = t;
+    __syncthreads();
+    float m = red32[0];
+#pragma unroll
+    for (int w2 = 1; w2 < kPT / 32; ++w2) m = fminf(m, red32[w2]);
+    sk.kind = P.skipk;
+    sk.thrmin = m;
+    return sk;
+}
+
 // =========================================================================
 // LSE half-sweep.  One side per launch (A.side[0]).
 // Stats written by the global finalizer: st[0] = residual ||a - X~ e||_1 of
@@ -538,7 +622,9 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
         }
     }
     float *dsc = dscr + tid * (kCC + 1);       // PC_SQTC: this thread's chunk distances
-    stream_columns<COST, DP>(P, i0, jb, je, inv_eta, 0, false, bufs, &tcs,
+    __shared__ float red32[kPT / 32];
+    const SkipCtx sk = skip_setup<DP>(P, rb, valid, thr_lo_of(mx - kLseCut), w_lo, red32);
+    const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, 0, false, bufs, &tcs, sk,
                              [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
         if (!valid) return;
         // phase 1 (branch-free): skip test against the chunk-start bound of the row max
@@ -591,6 +677,7 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
         }
     });
     if constexpr (COST == PC_SQTC) tc_teardown(tcs);
+    skip_count(P, sk, nskip, jb, je);
     if (valid) {
         P.pa[(long long)sp * P.M + i] = mx;
         P.pb[(long long)sp * P.M + i] = sm;
@@ -642,6 +729,7 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
         A.st[0] = R;
         A.st[1] = DM;
         if (A.count_sweep) A.ctl[1] += 1;
+        skip_switch(P);
         if (A.test_tol && A.sink_tol && R <= *A.sink_tol) {
             A.ctl[0] = 1;     // converged at the starting iterate: roll back this update
             A.ctl[2] = 1;
@@ -686,7 +774,9 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
     int cnt = 0;
     const long long bufbase = (i * P.S + sp) * P.cap;
     float *dsc = dscr + tid * (kCC + 1);
-    stream_columns<COST, DP>(P, i0, jb, je, inv_eta, P.m1_row ? 0 : 1, trial, bufs, &tcs,
+    __shared__ float red32[kPT / 32];
+    const SkipCtx sk = skip_setup<DP>(P, rb, valid, thr32, w_lo, red32);
+    const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, P.m1_row ? 0 : 1, trial, bufs, &tcs, sk,
                              [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
         if (!valid) return;
         unsigned mask = 0u;
@@ -745,6 +835,7 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
         }
     });
     if constexpr (COST == PC_SQTC) tc_teardown(tcs);
+    skip_count(P, sk, nskip, jb, je);
     if (valid) {
         P.pa[(long long)sp * P.M + i] = acc;
         if (sparse) P.cnt[i * P.S + sp] = cnt;
@@ -870,6 +961,7 @@ __global__ void __launch_bounds__(kPT) sum_pass_kernel(PassArgs A) {
         A.st[9] = Mr;
         A.st[10] = Mc;
         A.st[11] = A.nsides > 1 ? v[1][6] : 0.0;
+        for (int s2 = 0; s2 < A.nsides; ++s2) skip_switch(A.side[s2]);
         // row-block bases of the CSR / CSC (sequential scan, RB is small)
         for (int s2 = 0; s2 < A.nsides; ++s2) {
             const PassSide &P = A.side[s2];
@@ -1014,6 +1106,44 @@ __global__ void to_half16_kernel(long long np, int dp, const float *x32, __half 
 // squared norms, and the exactness facts the host needs to pick the fp32 path:
 // info[0] = max |coord| (as ordered bits), info[1] = max squared norm,
 // info[2] = number of non-integer coordinates.
+// Bounding boxes of consecutive groups of gsz points (fp32 copies, dp padded):
+// box[g] = [lo[0..dp), hi[0..dp)].  One thread per (group, dimension).
+__global__ void box_kernel(long long np, int dp, int gsz, const float *p32, float *box) {
+    const long long ng = (np + gsz - 1) / gsz;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ng * dp;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long g = t / dp;
+        const int k = (int)(t - g * dp);
+        const long long p0 = g * gsz, p1 = min(np, p0 + gsz);
+        float lo = INFINITY, hi = -INFINITY;
+        for (long long p = p0; p < p1; ++p) {
+            const float v = p32[p * dp + k];
+            lo = fminf(lo, v);
+            hi = fmaxf(hi, v);
+        }
+        box[g * 2 * dp + k] = lo;
+        box[g * 2 * dp + dp + k] = hi;
+    }
+}
+
+// Dmin table: lower bound of the distance between row block rb's box and column
+// group g's box (exact for integer points: fp64 sum of integer gaps, rounded
+// down to fp32).  kind 1 squared Euclidean, 2 L1.
+__global__ void dmin_kernel(long long RB, long long NG, int dp, int kind, const float *rbox, const float *cbox,
+                            float *dmin) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < RB * NG;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long rb = t / NG, g = t - rb * NG;
+        const float *R = rbox + rb * 2 * dp, *Cb = cbox + g * 2 * dp;
+        double s = 0.0;
+        for (int k = 0; k < dp; ++k) {
+            const double gap = fmax(0.0, fmax((double)Cb[k] - (double)R[dp + k], (double)R[k] - (double)Cb[dp + k]));
+            s += kind == 1 ? gap * gap : gap;
+        }
+        dmin[t] = __double2float_rd(s);
+    }
+}
+
 __global__ void prep_points_kernel(long long np, int d, int dp, const double *x, float *x32, double *x64,
                                    float *n32, unsigned long long *info) {
     double amax = 0.0, nmax = 0.0;

@@ -360,3 +360,39 @@ def test_tensor_core_cross_term_bit_identical(P, name, mk, monkeypatch):
     for x, y in zip(a[4], b[4]):
         assert np.array_equal(x, y)
     assert np.array_equal(a[5], b[5]) and np.array_equal(a[6], b[6])
+
+
+@pytest.mark.parametrize("name,mk", [("c3s", lambda: make("c3_gmm10k", scale=0.05)),
+                                     ("c4s", lambda: make("c4_l1rect", scale=0.05)),
+                                     ("rag_sq", lambda: ragged(301, 517, 9, "sq", 10)),
+                                     ("rag_l1", lambda: ragged(517, 301, 3, "l1", 11))])
+def test_tile_skip_bit_identical(P, name, mk, monkeypatch):
+    # whole-chunk skipping (R10, tile form) drops a chunk only when the box bound proves
+    # that the per-entry fp32 test rejects every entry of it, so every pass must be
+    # bit-identical with and without it; whole solves agree to rounding (the tree
+    # preconditioner's shared-memory atomics make CG sums order-dependent run to run)
+    w = mk()
+    C, Ck, phi, psi, s, f, g = oracle_state(w, 1)
+    tau = 1e-4 / (w.m * w.n)
+    out = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("PINS_NO_TILESKIP", "1")
+        pb = P.DeviceProblem.from_workload(w)
+        ws = P.Workspace()
+        ev = P.evaluate(ws, pb, T(phi), T(psi), s, T(f), T(g), tau=tau)
+        csr = [H(t) for t in P.get_csr(ws)]
+        fd, gd = T(f), T(g)
+        for _ in range(3):
+            P.sinkhorn_sweep(ws, pb, T(phi), T(psi), s, fd, gd)
+        r = P.solve(pb, P.default_params(K=6, outer_tol=0.0))
+        out.append((H(ev["r"]), H(ev["c"]), ev["cost"], ev["grad_l1"], csr, H(fd), H(gd),
+                    r["obj"], H(r["u"]), H(r["v"])))
+    a, b = out
+    for x, y in zip(a[:2], b[:2]):
+        assert np.array_equal(x, y)
+    assert a[2] == b[2] and a[3] == b[3]
+    for x, y in zip(a[4], b[4]):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a[5], b[5]) and np.array_equal(a[6], b[6])
+    assert abs(a[7] - b[7]) <= 1e-9 * abs(b[7])
