@@ -6,7 +6,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc", "pins_api.cu")
-DEPS = [os.path.join(PKG, "csrc", f) for f in ("pins_api.cu", "pins_kernels.cuh", "pins_device.cuh")]
+CSRC = os.path.join(PKG, "csrc")
+DEPS = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh", ".h"))]
 HDR = os.path.join(ROOT, "include", "pins.h")
 LIB = os.path.join(PKG, "libpins_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -158,8 +158,7 @@ struct pins_workspace {
     // v2 dense passes
     SideBufs sb[2];
     DevBuf x32, y32, x64, y64, nx32, ny32, xh, yh, pinfo, ctl, gticket, pst, tol;
-    DevBuf bx128, bx32, by128, by32;    // tile-skip boxes (row blocks / column groups)
-    DevBuf dmin0, dmin1, skst;          // Dmin tables per orientation, adaptive switch states
+    DevBuf sk_gam[4], sk_tref[4], sk_qref[4], skst;   // chunk-skip certificates: (LSE, SUM) x orientation
     const void *key_C = nullptr, *key_x = nullptr, *key_y = nullptr;
     long long key_m = -1, key_n = -1, key_ldc = -1;
     int key_kind = -1, key_d = -1;
@@ -550,6 +549,7 @@ int prepare_pass(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
     if (pb->cost_kind == PINS_COST_DENSE) {
         ws->cost_row = PC_DENSE_ROW;
         ws->cost_col = PC_DENSE_COL;
+        ws->skipk = 0;
         ws->dp = 4;
     } else {
         const int dp = dp_for(pb->d);
@@ -595,38 +595,35 @@ int prepare_pass(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
             exact32 = integral && 2.0 * pb->d * std::max(ax, ay) < two24;
             ws->cost_row = ws->cost_col = exact32 ? PC_L132 : PC_L164;
         }
-        // tile skipping needs exact fp32 distances (integer points, R10)
-        ws->skipk = 0;
-        if (exact32 && getenv("PINS_NO_TILESKIP") == nullptr) {
-            ws->skipk = pb->cost_kind == PINS_COST_SQEUCLID ? 1 : 2;
-            const long long gx128 = (m + kPT - 1) / kPT, gy128 = (n + kPT - 1) / kPT;
-            const long long gx32 = (m + kCC - 1) / kCC, gy32 = (n + kCC - 1) / kCC;
-            PINS_TRY(ensure(ws->bx128, sizeof(float) * gx128 * 2 * dp));
-            PINS_TRY(ensure(ws->by128, sizeof(float) * gy128 * 2 * dp));
-            PINS_TRY(ensure(ws->bx32, sizeof(float) * gx32 * 2 * dp));
-            PINS_TRY(ensure(ws->by32, sizeof(float) * gy32 * 2 * dp));
-            LAUNCH(PINS_PROF_VEC, st, box_kernel<<<grid_1d(gx128 * dp, ws->nsm), 256, 0, st>>>(
-                m, dp, kPT, ptr<float>(ws->x32), ptr<float>(ws->bx128)));
-            LAUNCH(PINS_PROF_VEC, st, box_kernel<<<grid_1d(gy128 * dp, ws->nsm), 256, 0, st>>>(
-                n, dp, kPT, ptr<float>(ws->y32), ptr<float>(ws->by128)));
-            LAUNCH(PINS_PROF_VEC, st, box_kernel<<<grid_1d(gx32 * dp, ws->nsm), 256, 0, st>>>(
-                m, dp, kCC, ptr<float>(ws->x32), ptr<float>(ws->bx32)));
-            LAUNCH(PINS_PROF_VEC, st, box_kernel<<<grid_1d(gy32 * dp, ws->nsm), 256, 0, st>>>(
-                n, dp, kCC, ptr<float>(ws->y32), ptr<float>(ws->by32)));
-            PINS_TRY(ensure(ws->dmin0, sizeof(float) * gx128 * gy32));
-            PINS_TRY(ensure(ws->dmin1, sizeof(float) * gy128 * gx32));
-            LAUNCH(PINS_PROF_VEC, st, dmin_kernel<<<grid_1d(gx128 * gy32, ws->nsm), 256, 0, st>>>(
-                gx128, gy32, dp, ws->skipk, ptr<float>(ws->bx128), ptr<float>(ws->by32), ptr<float>(ws->dmin0)));
-            LAUNCH(PINS_PROF_VEC, st, dmin_kernel<<<grid_1d(gy128 * gx32, ws->nsm), 256, 0, st>>>(
-                gy128, gx32, dp, ws->skipk, ptr<float>(ws->by128), ptr<float>(ws->bx32), ptr<float>(ws->dmin1)));
-            PINS_TRY(ensure(ws->skst, sizeof(int) * 16));
-            PINS_CUDA(cudaMemsetAsync(ws->skst.p, 0, sizeof(int) * 16, st));
-            PINS_CUDA(cudaGetLastError());
+        // chunk skipping needs exact fp32 distances (integer points, R10)
+        ws->skipk = exact32 && getenv("PINS_NO_TILESKIP") == nullptr ? 1 : 0;
+    }
+    if (ws->skipk) {
+        for (int q = 0; q < 4; ++q) {
+            const int o = q & 1;
+            const long long M = o == 0 ? m : n, N = o == 0 ? n : m;
+            const long long RB = (M + kPT - 1) / kPT, S = ws->S[o];
+            const long long cps = ((N + S - 1) / S + kCC - 1) / kCC + 1;
+            PINS_TRY(ensure(ws->sk_gam[q], sizeof(float) * RB * S * cps * 4));
+            PINS_TRY(ensure(ws->sk_tref[q], sizeof(float) * M));
+            PINS_TRY(ensure(ws->sk_qref[q], sizeof(float) * N));
         }
+        PINS_TRY(ensure(ws->skst, sizeof(int) * 32));
+        PINS_CUDA(cudaMemsetAsync(ws->skst.p, 0xff, sizeof(int) * 32, st));   // age -1: record first
     }
     ws->key_C = pb->C; ws->key_x = pb->x; ws->key_y = pb->y; ws->key_m = m; ws->key_n = n;
     ws->key_kind = pb->cost_kind; ws->key_d = pb->d; ws->key_ldc = pb->ldc;
     return PINS_OK;
+}
+
+// chunk-skip state q = 2 * (0 LSE, 1 SUM) + orientation
+void set_skip(pins_workspace *ws, PassSide &P, int q) {
+    if (!P.skipk) return;
+    P.cps = (int)(((P.N + P.S - 1) / P.S + kCC - 1) / kCC + 1);
+    P.gam = ptr<float>(ws->sk_gam[q]);
+    P.tref = ptr<float>(ws->sk_tref[q]);
+    P.qref = ptr<float>(ws->sk_qref[q]);
+    P.skst = ptr<int>(ws->skst) + 8 * q;
 }
 
 // Fill the pass description of one orientation (0: rows of X, 1: columns).
@@ -650,9 +647,7 @@ void fill_side(pins_workspace *ws, const pins_problem *pb, int o, const double *
     P.xrh = ptr<__half>(row ? ws->xh : ws->yh);
     P.ych = ptr<__half>(row ? ws->yh : ws->xh);
     P.skipk = pb->cost_kind == PINS_COST_DENSE ? 0 : ws->skipk;
-    P.dmin = ptr<float>(row ? ws->dmin0 : ws->dmin1);
-    P.ng = (P.N + kCC - 1) / kCC;
-    P.skst = ptr<int>(ws->skst) + 4 * (2 + o);     // sum passes; half_sweep uses states 0 / 1
+    set_skip(ws, P, 2 + o);      // sum passes; half_sweep switches to the LSE state o
     P.fr = row ? f : g;
     P.phir = row ? phi : psi;
     P.gc = row ? g : f;
@@ -732,7 +727,7 @@ int half_sweep(pins_workspace *ws, const pins_problem *pb, int o, const double *
     PassArgs A;
     base_args(ws, pb, s, A);
     fill_side(ws, pb, o, f, phi, g, psi, A.side[0]);
-    A.side[0].skst = ptr<int>(ws->skst) + 4 * o;
+    set_skip(ws, A.side[0], o);
     A.side[0].fout = o == 0 ? f : g;
     A.side[0].fsave = o == 0 ? ptr<double>(ws->fsave) : nullptr;
     A.nsides = 1;

@@ -67,10 +67,15 @@ struct PassSide {
     const __half *xrh, *ych;        // PC_SQTC: fp16 points, M x 16 / N x 16 (zero padded)
     // tile skipping (exact-fp32 point costs): bounding boxes [lo[dp], hi[dp]] of the
     // pass rows per row block (kPT rows) and of the pass columns per group of kCC
-    int skipk;                      // 0 off, 1 squared Euclidean, 2 L1
-    const float *dmin;              // [RB x ceil(N / kCC)]: box distance lower bound (rounded down)
-    long long ng;                   // ceil(N / kCC)
-    int *skst;                      // adaptive switch: [0] passes left disabled, [1] skipped, [2] chunks
+    // chunk skipping by drift certificates (SkipCtx; exact-fp32 point costs only)
+    int skipk;                      // 0 off, 1 on
+    int cps;                        // chunks per split (upper bound)
+    float *gam;                     // [RB * S * cps * 4]: certificate per (row block, split, chunk, warp)
+    float *tref;                    // [M]: reference-pass row thresholds
+    float *qref;                    // [N]: reference-pass skip-test column values
+    int *skst;                      // [0] age (< 0: next pass records), [1] skipped, [2] chunks,
+                                    // [3] w_lo of the reference (float bits), [4] best skip fraction (ppm),
+                                    // [5] passes left switched off
     // potentials: pass-row side (fr + phir), pass-column side (gc + psic)
     const double *fr, *phir, *gc, *psic;
     int m1_row;                     // SUM: the "-1" of Eq. (7) sits on the pass-row potential
@@ -156,16 +161,26 @@ struct Buf {
 template <int COST>
 constexpr int kNBuf = COST == PC_DENSE_ROW ? 1 : 2;
 
-// Whole-chunk skip (R10, tile form).  With integer points every fp32 distance Df
-// is exact, so Df >= Dmin, the distance between the row block's box and the
-// chunk's box.  If  max_c qs_c - w_lo Dmin <= min_i thr32_i  then no entry of the
-// chunk passes the per-entry fp32 test (fl is monotone and thr32 representable),
-// so skipping the chunk changes nothing: results are bit-identical with and
-// without it.  thrmin is a lower bound of every row's thr32 over the whole pass.
+// Whole-chunk skip by drift certificates (R10, tile form).  An entry passes the
+// per-entry fp32 test iff fl(qs_j - w_lo Df_ij) > thr32_i, i.e. (fl monotone,
+// thr32 representable) only if the real value qs_j - w_lo Df_ij > thr32_i.  With
+// integer points Df_ij is exact and the same in every pass.  A reference pass
+// records, per (row block, split, chunk), gamma >= max_i (max_j v_ij + |v| 2^-22
+// - T_i) with v the fp32 test values, T_i = the row's threshold then, and qref_j =
+// the column values then.  In a later pass with w_lo >= w_lo(ref),
+//     qs_j - w_lo Df_ij <= v_ij(real) + (qs_j - qref_j) <= gamma + T_i + max_j (qs_j - qref_j),
+// so if  gamma + max_j (qs_j - qref_j) <= min_i (thr32_i - T_i)  no entry of the
+// chunk can pass and the chunk is skipped: results are bit-identical with and
+// without skipping.  The potentials drift slowly between passes, so certificates
+// stay valid for many passes; a pass records fresh ones when the skip fraction
+// falls (skip_switch).
 struct SkipCtx {
-    int kind;                   // 0: never skip
-    float thrmin, w_lo;
-    const float *drow;          // the row block's row of the Dmin table
+    int kind;                   // 0 off, 1 test certificates, 2 record (reference pass)
+    double dthr;                // kind 1: min over the CTA's rows of thr32_i - T_i (rounded down)
+    long long jb;               // the CTA's first column
+    float *gcta;                // the CTA's certificates [cps * 4]
+    float *qref;
+    bool wq;                    // kind 2: this CTA writes qref (row block 0)
 };
 
 template <int COST, int DP>
@@ -174,15 +189,21 @@ struct Pref {
     static constexpr bool PTS64 = COST == PC_SQ64 || COST == PC_L164;
     static constexpr int NY = (PTS32 || PTS64) ? (kCC * DP + kPT - 1) / kPT : 1;
     double g, psi, ev, bv;
-    float ny, dm;                                // owner warp lane 0: the chunk's Dmin
+    float ny, qr, gm;                            // owner warp: qref of the lane's column, certificate
     float y32[PTS32 ? NY : 1];
     double y64[PTS64 ? NY : 1];
     uint2 yh;
     // global -> registers (this thread's share of columns j0 .. j0+nc-1)
     __device__ __forceinline__ void load(const PassSide &P, long long j0, int nc, bool trial, const SkipCtx &sk) {
         const int tid = threadIdx.x;
-        if (sk.kind && tid == (trial ? kCC : 0) && nc > 0)
-            dm = fminf(__ldg(sk.drow + j0 / kCC), __ldg(sk.drow + (j0 + nc - 1) / kCC));
+        if (sk.kind == 1 && (tid >> 5) == (trial ? 1 : 0)) {
+            const int lane = tid & 31;
+            qr = lane < nc ? __ldg(sk.qref + j0 + lane) : 0.f;
+            if (lane == 0) {
+                const float4 g4 = __ldg(reinterpret_cast<const float4 *>(sk.gcta + ((j0 - sk.jb) / kCC) * 4));
+                gm = fmaxf(fmaxf(g4.x, g4.y), fmaxf(g4.z, g4.w));
+            }
+        }
         if (tid < kCC) {
             const bool ok = tid < nc;
             g = ok ? P.gc[j0 + tid] : 0.0;
@@ -220,16 +241,22 @@ struct Pref {
             }
         }
     }
-    // owner warp: the chunk skip decision from this lane's qs value (all 32 lanes)
-    __device__ __forceinline__ void decide(Buf<COST, DP> &B, const SkipCtx &sk, float qs) const {
+    // owner warp (all 32 lanes; lane = column of the chunk): the chunk skip decision,
+    // or in a reference pass the record of the column values
+    __device__ __forceinline__ void decide(Buf<COST, DP> &B, const SkipCtx &sk, float qs, long long j0,
+                                           int nc) const {
         const int lane = threadIdx.x & 31;
-        float qm = qs;
+        if (sk.kind == 1) {
+            double d = qs == -INFINITY ? -INFINITY : (double)qs - (double)qr;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
-        if (lane == 0) {
-            const double wd = (double)sk.w_lo * (double)dm;
-            const double lhs = (double)qm - wd;
-            B.skip = lhs + 1e-14 * (fabs((double)qm) + wd) <= (double)sk.thrmin;
+            for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+            if (lane == 0) {
+                const double g = (double)gm, lhs = g + d - sk.dthr;
+                B.skip = lhs + 1e-12 * (fabs(g) + fabs(d) + fabs(sk.dthr)) <= 0.0;
+            }
+        } else {
+            if (sk.kind == 2 && sk.wq && lane < nc) sk.qref[j0 + lane] = qs;
+            if (lane == 0) B.skip = 0;
         }
     }
     // registers -> shared buffer.  qmode: 0 q = (g+psi)/eta, 1 q = (g+psi)/eta - 1
@@ -244,8 +271,7 @@ struct Pref {
                 const float qs = qs_of(q);
                 B.qt[tid] = q;
                 B.qs[tid] = qs;
-                if (sk.kind) decide(B, sk, qs);
-                else if (tid == 0) B.skip = 0;
+                decide(B, sk, qs, j0, nc);
             } else if (tid == 0) B.skip = 0;
         } else if (tid < 2 * kCC && trial) {
             B.ev[tid - kCC] = ev;
@@ -280,7 +306,7 @@ struct Pref {
         }
     }
     // trial: the skip-test value q + bv needs q, written by threads < kCC
-    __device__ __forceinline__ void store_trial_qt(Buf<COST, DP> &B, const SkipCtx &sk) {
+    __device__ __forceinline__ void store_trial_qt(Buf<COST, DP> &B, const SkipCtx &sk, long long j0, int nc) {
         const int tid = threadIdx.x;
         if (tid >= kCC && tid < 2 * kCC) {
             const int c = tid - kCC;
@@ -288,7 +314,7 @@ struct Pref {
             const float qs = qs_of(qt);
             B.qt[c] = qt;
             B.qs[c] = qs;
-            if (sk.kind) decide(B, sk, qs);
+            decide(B, sk, qs, j0, nc);
         }
     }
 };
@@ -418,7 +444,7 @@ __device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, l
     // prologue: chunk 0 into buffer 0, prefetch chunk 1
     pf.load(P, jb, nc_of(0), trial, sk);
     pf.store(bufs[0], P, i0, jb, nc_of(0), inv_eta, qmode, trial, sk);
-    if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0], sk); }
+    if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0], sk, jb, nc_of(0)); }
     if (NB > 1 && nch > 1) pf.load(P, jb + kCC, nc_of(1), trial, sk);
     if constexpr (COST == PC_SQTC) tc::fence_proxy_async();
     __syncthreads();
@@ -436,7 +462,7 @@ __device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, l
             if constexpr (COST == PC_SQTC) tc::fence_before();
             __syncthreads();                         // chunk c-1 fully consumed
             pf.store(bufs[nxt], P, i0, jb + (c + 1) * kCC, nc_of(c + 1), inv_eta, qmode, trial, sk);
-            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[nxt], sk); }
+            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[nxt], sk, jb + (c + 1) * kCC, nc_of(c + 1)); }
             if (c + 2 < nch) pf.load(P, jb + (c + 2) * kCC, nc_of(c + 2), trial, sk);
             if constexpr (COST == PC_SQTC) tc::fence_proxy_async();
             __syncthreads();
@@ -451,7 +477,7 @@ __device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, l
             __syncthreads();
             pf.load(P, jb + c * kCC, nc_of(c), trial, sk);
             pf.store(bufs[0], P, i0, jb + c * kCC, nc_of(c), inv_eta, qmode, trial, sk);
-            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0], sk); }
+            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0], sk, jb + c * kCC, nc_of(c)); }
             __syncthreads();
         }
         if (bufs[cur].skip) { ++nskip; continue; }   // read before the next chunk boundary's barrier
@@ -471,16 +497,35 @@ __device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, l
 // that skipped < 5 % of its chunks turns skipping off for the next 16 passes
 __device__ __forceinline__ void skip_count(const PassSide &P, const SkipCtx &sk, int nskip, long long jb,
                                            long long je) {
-    if (threadIdx.x == 0 && sk.kind) {
+    if (threadIdx.x == 0 && sk.kind == 1) {
         atomicAdd(P.skst + 1, nskip);
         atomicAdd(P.skst + 2, (int)((je - jb + kCC - 1) / kCC));
     }
 }
-__device__ __forceinline__ void skip_switch(const PassSide &P) {
+__device__ __forceinline__ bool skip_is_ref(const PassSide &P, float w_lo) {
+    return P.skst[0] < 0 || !(w_lo >= __int_as_float(P.skst[3]));
+}
+// launch finalizer: after a reference pass start a new period; afterwards record fresh
+// certificates once the skip fraction falls below 3/4 of the period's best (or at age
+// 64); a pass that skipped < 5 % switches skipping off for 16 passes, then re-records
+__device__ __forceinline__ void skip_switch(const PassSide &P, float w_lo) {
     if (!P.skipk) return;
     int *s = P.skst;
-    if (s[0] > 0) { s[0] -= 1; return; }
-    s[0] = (20LL * s[1] < (long long)s[2]) ? 16 : 0;
+    if (s[5] > 0) {
+        if (--s[5] == 0) s[0] = -1;
+        return;
+    }
+    if (skip_is_ref(P, w_lo)) {
+        s[0] = 1;
+        s[3] = __float_as_int(w_lo);
+        s[4] = -1;
+    } else {
+        const int frac = s[2] > 0 ? (int)(1e6 * (double)s[1] / (double)s[2]) : 0;
+        s[4] = max(s[4], frac);
+        s[0] += 1;
+        if (frac < 50000) s[5] = 16;
+        else if (4LL * frac < 3LL * s[4] || s[0] > 64) s[0] = -1;
+    }
     s[1] = 0;
     s[2] = 0;
 }
@@ -564,25 +609,72 @@ __device__ __forceinline__ double block_reduce_max(double v, double *sh) {
     return t;
 }
 
-// CTA setup of the chunk skip: the minimum over the CTA's valid rows of the fp32 threshold (block-wide; contains
-// __syncthreads, call from all threads).
-template <int DP>
-__device__ __forceinline__ SkipCtx skip_setup(const PassSide &P, int rb, bool valid, float thr32, float w_lo,
-                                              float *red32) {
-    SkipCtx sk{0, -INFINITY, w_lo, P.dmin + (long long)rb * P.ng};
-    if (!P.skipk || P.skst[0] > 0) return sk;     // off, or switched off for this pass
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    float t = valid ? thr32 : INFINITY;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t = fminf(t, __shfl_xor_sync(0xffffffffu, t, o));
-    if (lane == 0) red32[warp] = t;
-    __syncthreads();
-    float m = red32[0];
-#pragma unroll
-    for (int w2 = 1; w2 < kPT / 32; ++w2) m = fminf(m, red32[w2]);
-    sk.kind = P.skipk;
-    sk.thrmin = m;
+// CTA setup of the chunk skip (block-wide; contains __syncthreads, call from all
+// threads).  thr32 = the row's threshold at the start of the pass.
+__device__ __forceinline__ SkipCtx skip_setup(const PassSide &P, int rb, int sp, long long i, bool valid,
+                                              long long jb, float thr32, float w_lo, double *red) {
+    SkipCtx sk{0, -INFINITY, jb, nullptr, P.qref, rb == 0};
+    if (!P.skipk || P.skst[5] > 0) return sk;
+    sk.gcta = P.gam + ((long long)rb * P.S + sp) * P.cps * 4;
+    if (skip_is_ref(P, w_lo)) {
+        sk.kind = 2;
+        if (valid && sp == 0) P.tref[i] = thr32;
+        return sk;
+    }
+    sk.kind = 1;
+    double d = INFINITY;
+    if (valid) {
+        const float t = P.tref[i];
+        d = thr32 == -INFINITY ? -INFINITY : (double)thr32 - (double)t;
+        d -= 1e-15 * (fabs((double)thr32) + fabs((double)t));
+    }
+    d = -block_reduce_max(-d, red);
+    sk.dthr = d;
     return sk;
+}
+
+// reference pass: certificate of this chunk for the warp's rows (all 32 lanes)
+__device__ __forceinline__ void record_cert(const SkipCtx &sk, long long j0, float vmx, float T, bool valid) {
+    double e = -INFINITY;
+    if (valid && vmx != -INFINITY) e = (double)vmx + fabs((double)vmx) * 0x1p-22 - (double)T;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+    if ((threadIdx.x & 31) == 0) sk.gcta[((j0 - sk.jb) / kCC) * 4 + (threadIdx.x >> 5)] = __double2float_ru(e);
+}
+
+// phase 1 of a chunk (branch-free): the survivor mask of the fp32 test
+// fl(qs_j - w_lo D_ij) > thr32, the fp32 distances (PC_SQTC) and the row's
+// maximum test value (used by reference passes)
+template <int COST, int DP>
+__device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSide &P, const RowPt<COST, DP> &rp,
+                                           long long i, long long j0, int nc, const float *dots, float w_lo,
+                                           float thr32, float (&Dv)[COST == PC_SQTC ? kCC : 1], float &vmx) {
+    unsigned mask = 0u;
+#pragma unroll
+    for (int c4 = 0; c4 < kCC; c4 += 4) {
+        const float4 qs4 = *reinterpret_cast<const float4 *>(B.qs + c4);
+        const float qsv[4] = {qs4.x, qs4.y, qs4.z, qs4.w};
+        float nyv[4] = {0.f, 0.f, 0.f, 0.f};
+        if constexpr (COST == PC_SQTC) {
+            const float4 ny4 = *reinterpret_cast<const float4 *>(B.ny + c4);
+            nyv[0] = ny4.x; nyv[1] = ny4.y; nyv[2] = ny4.z; nyv[3] = ny4.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = c4 + j;
+            float Df;
+            if constexpr (COST == PC_SQTC) {
+                Df = fmaf(-2.f, dots[c], rp.nx + nyv[j]);
+                Dv[c] = Df;
+            } else {
+                Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+            }
+            const float v = fmaf(-w_lo, Df, qsv[j]);
+            vmx = c < nc ? fmaxf(vmx, v) : vmx;
+            mask |= (c < nc && v > thr32) ? (1u << c) : 0u;
+        }
+    }
+    return mask;
 }
 
 // =========================================================================
@@ -622,37 +714,19 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
         }
     }
     float *dsc = dscr + tid * (kCC + 1);       // PC_SQTC: this thread's chunk distances
-    __shared__ float red32[kPT / 32];
-    const SkipCtx sk = skip_setup<DP>(P, rb, valid, thr_lo_of(mx - kLseCut), w_lo, red32);
+    const float thr0 = thr_lo_of(mx - kLseCut);
+    const SkipCtx sk = skip_setup(P, rb, sp, i, valid, jb, thr0, w_lo, red);
     const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, 0, false, bufs, &tcs, sk,
                              [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
-        if (!valid) return;
-        // phase 1 (branch-free): skip test against the chunk-start bound of the row max
+        // phase 1: skip test against the chunk-start bound of the row max
         const float thr32 = thr_lo_of(mx - kLseCut);
         unsigned mask = 0u;
+        float vmx = -INFINITY;
         float Dv[COST == PC_SQTC ? kCC : 1];
-#pragma unroll
-        for (int c4 = 0; c4 < kCC; c4 += 4) {
-            const float4 qs4 = *reinterpret_cast<const float4 *>(B.qs + c4);
-            const float qsv[4] = {qs4.x, qs4.y, qs4.z, qs4.w};
-            float nyv[4] = {0.f, 0.f, 0.f, 0.f};
-            if constexpr (COST == PC_SQTC) {
-                const float4 ny4 = *reinterpret_cast<const float4 *>(B.ny + c4);
-                nyv[0] = ny4.x; nyv[1] = ny4.y; nyv[2] = ny4.z; nyv[3] = ny4.w;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int c = c4 + j;
-                float Df;
-                if constexpr (COST == PC_SQTC) {
-                    Df = fmaf(-2.f, dots[c], rp.nx + nyv[j]);
-                    Dv[c] = Df;
-                } else {
-                    Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c);
-                }
-                mask |= (c < nc && fmaf(-w_lo, Df, qsv[j]) > thr32) ? (1u << c) : 0u;
-            }
-        }
+        if (valid)
+            mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx);
+        if (sk.kind == 2) record_cert(sk, j0, vmx, thr0, valid);
+        if (!valid) return;
         if constexpr (COST == PC_SQTC) {
             // distances are needed only where some lane of the warp has a survivor
             if (__any_sync(__activemask(), mask != 0u)) {
@@ -729,7 +803,7 @@ __global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
         A.st[0] = R;
         A.st[1] = DM;
         if (A.count_sweep) A.ctl[1] += 1;
-        skip_switch(P);
+        skip_switch(P, w_lo);
         if (A.test_tol && A.sink_tol && R <= *A.sink_tol) {
             A.ctl[0] = 1;     // converged at the starting iterate: roll back this update
             A.ctl[2] = 1;
@@ -774,35 +848,16 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
     int cnt = 0;
     const long long bufbase = (i * P.S + sp) * P.cap;
     float *dsc = dscr + tid * (kCC + 1);
-    __shared__ float red32[kPT / 32];
-    const SkipCtx sk = skip_setup<DP>(P, rb, valid, thr32, w_lo, red32);
+    const SkipCtx sk = skip_setup(P, rb, sp, i, valid, jb, thr32, w_lo, red);
     const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, P.m1_row ? 0 : 1, trial, bufs, &tcs, sk,
                              [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
-        if (!valid) return;
         unsigned mask = 0u;
+        float vmx = -INFINITY;
         float Dv[COST == PC_SQTC ? kCC : 1];
-#pragma unroll
-        for (int c4 = 0; c4 < kCC; c4 += 4) {
-            const float4 qs4 = *reinterpret_cast<const float4 *>(B.qs + c4);
-            const float qsv[4] = {qs4.x, qs4.y, qs4.z, qs4.w};
-            float nyv[4] = {0.f, 0.f, 0.f, 0.f};
-            if constexpr (COST == PC_SQTC) {
-                const float4 ny4 = *reinterpret_cast<const float4 *>(B.ny + c4);
-                nyv[0] = ny4.x; nyv[1] = ny4.y; nyv[2] = ny4.z; nyv[3] = ny4.w;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int c = c4 + j;
-                float Df;
-                if constexpr (COST == PC_SQTC) {
-                    Df = fmaf(-2.f, dots[c], rp.nx + nyv[j]);
-                    Dv[c] = Df;
-                } else {
-                    Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c);
-                }
-                mask |= (c < nc && fmaf(-w_lo, Df, qsv[j]) > thr32) ? (1u << c) : 0u;
-            }
-        }
+        if (valid)
+            mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx);
+        if (sk.kind == 2) record_cert(sk, j0, vmx, thr32, valid);
+        if (!valid) return;
         if constexpr (COST == PC_SQTC) {
             // distances are needed only where some lane of the warp has a survivor
             if (__any_sync(__activemask(), mask != 0u)) {
@@ -961,7 +1016,8 @@ __global__ void __launch_bounds__(kPT) sum_pass_kernel(PassArgs A) {
         A.st[9] = Mr;
         A.st[10] = Mc;
         A.st[11] = A.nsides > 1 ? v[1][6] : 0.0;
-        for (int s2 = 0; s2 < A.nsides; ++s2) skip_switch(A.side[s2]);
+        const float wl = (float)A.w * (1.f - 0x1p-19f);
+        for (int s2 = 0; s2 < A.nsides; ++s2) skip_switch(A.side[s2], wl);
         // row-block bases of the CSR / CSC (sequential scan, RB is small)
         for (int s2 = 0; s2 < A.nsides; ++s2) {
             const PassSide &P = A.side[s2];
@@ -1106,44 +1162,6 @@ __global__ void to_half16_kernel(long long np, int dp, const float *x32, __half 
 // squared norms, and the exactness facts the host needs to pick the fp32 path:
 // info[0] = max |coord| (as ordered bits), info[1] = max squared norm,
 // info[2] = number of non-integer coordinates.
-// Bounding boxes of consecutive groups of gsz points (fp32 copies, dp padded):
-// box[g] = [lo[0..dp), hi[0..dp)].  One thread per (group, dimension).
-__global__ void box_kernel(long long np, int dp, int gsz, const float *p32, float *box) {
-    const long long ng = (np + gsz - 1) / gsz;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ng * dp;
-         t += (long long)gridDim.x * blockDim.x) {
-        const long long g = t / dp;
-        const int k = (int)(t - g * dp);
-        const long long p0 = g * gsz, p1 = min(np, p0 + gsz);
-        float lo = INFINITY, hi = -INFINITY;
-        for (long long p = p0; p < p1; ++p) {
-            const float v = p32[p * dp + k];
-            lo = fminf(lo, v);
-            hi = fmaxf(hi, v);
-        }
-        box[g * 2 * dp + k] = lo;
-        box[g * 2 * dp + dp + k] = hi;
-    }
-}
-
-// Dmin table: lower bound of the distance between row block rb's box and column
-// group g's box (exact for integer points: fp64 sum of integer gaps, rounded
-// down to fp32).  kind 1 squared Euclidean, 2 L1.
-__global__ void dmin_kernel(long long RB, long long NG, int dp, int kind, const float *rbox, const float *cbox,
-                            float *dmin) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < RB * NG;
-         t += (long long)gridDim.x * blockDim.x) {
-        const long long rb = t / NG, g = t - rb * NG;
-        const float *R = rbox + rb * 2 * dp, *Cb = cbox + g * 2 * dp;
-        double s = 0.0;
-        for (int k = 0; k < dp; ++k) {
-            const double gap = fmax(0.0, fmax((double)Cb[k] - (double)R[dp + k], (double)R[k] - (double)Cb[dp + k]));
-            s += kind == 1 ? gap * gap : gap;
-        }
-        dmin[t] = __double2float_rd(s);
-    }
-}
-
 __global__ void prep_points_kernel(long long np, int d, int dp, const double *x, float *x32, double *x64,
                                    float *n32, unsigned long long *info) {
     double amax = 0.0, nmax = 0.0;
