@@ -892,11 +892,13 @@ int build_csc(pins_workspace *ws, long long m, long long n, const long long *row
     return PINS_OK;
 }
 
-int cg_blocks(pins_workspace *ws, long long N) {
+int cg_blocks(pins_workspace *ws, long long N, bool vec = false) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_kernel, kThreads, 0);
-    per_sm = std::max(1, std::min(per_sm, 2));
-    long long want = (N + kThreads - 1) / kThreads;
+    // thread per row: one CTA per 256 rows; warp per row (vec): one warp per row, up to
+    // 4 CTAs per SM (the per-iteration grid reductions read one partial per CTA)
+    per_sm = std::max(1, std::min(per_sm, vec ? 4 : 2));
+    long long want = vec ? (N * 32 + kThreads - 1) / kThreads : (N + kThreads - 1) / kThreads;
     return (int)std::max<long long>(1, std::min<long long>(want, (long long)ws->nsm * per_sm));
 }
 
@@ -907,7 +909,8 @@ int run_cg(pins_workspace *ws, long long m, long long n, const long long *rowptr
            const double *gradg, const double *a, const double *b, cudaStream_t st, long long nnz_hint = -1) {
     const long long N = m + n;
     PINS_TRY(ensure(ws->cgvec, sizeof(double) * 4 * N));
-    const int G = cg_blocks(ws, N);
+    const bool vec = (double)(nnz_hint >= 0 ? nnz_hint : ws->nnz) > 8.0 * (double)N;
+    const int G = cg_blocks(ws, N, vec);
     PINS_TRY(ensure(ws->cgpart, sizeof(double) * 4 * G));
     PINS_TRY(ensure(ws->cgst, sizeof(double) * 8));
     CGArgs A;
@@ -937,7 +940,7 @@ int run_cg(pins_workspace *ws, long long m, long long n, const long long *rowptr
     A.a = a;
     A.b = b;
     A.st = ptr<double>(ws->cgst);
-    A.vec = (double)(nnz_hint >= 0 ? nnz_hint : ws->nnz) > 8.0 * (double)N ? 1 : 0;
+    A.vec = vec ? 1 : 0;
     void *args[] = {&A};
     cudaError_t e_cg = cudaSuccess;
     LAUNCH(PINS_PROF_CG, st, e_cg = cudaLaunchCooperativeKernel((void *)cg_kernel, dim3(G), dim3(kThreads), args, 0, st));

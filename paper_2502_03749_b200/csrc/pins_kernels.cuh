@@ -522,6 +522,7 @@ __device__ __forceinline__ double grid_reduce(const double *part, int slot, int 
     __syncthreads();
     if (threadIdx.x < 32) {
         double t = 0.0;
+#pragma unroll 8
         for (int b2 = threadIdx.x; b2 < G; b2 += 32) t += __ldcg(part + b2 * 4 + slot);
         t = warp_sum(t);
         if (threadIdx.x == 0) bcast = t;
