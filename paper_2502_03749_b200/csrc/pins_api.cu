@@ -608,8 +608,10 @@ int prepare_pass(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
             PINS_TRY(ensure(ws->sk_tref[q], sizeof(float) * M));
             PINS_TRY(ensure(ws->sk_qref[q], sizeof(float) * N));
         }
-        PINS_TRY(ensure(ws->skst, sizeof(int) * 32));
-        PINS_CUDA(cudaMemsetAsync(ws->skst.p, 0xff, sizeof(int) * 32, st));   // age -1: record first
+        PINS_TRY(ensure(ws->skst, sizeof(int) * 64));
+        PINS_CUDA(cudaMemsetAsync(ws->skst.p, 0xff, sizeof(int) * 64, st));   // age -1: record first
+        for (int q = 0; q < 4; ++q)
+            PINS_CUDA(cudaMemsetAsync(ptr<int>(ws->skst) + 16 * q + 6, 0, sizeof(int) * 4, st));
     }
     ws->key_C = pb->C; ws->key_x = pb->x; ws->key_y = pb->y; ws->key_m = m; ws->key_n = n;
     ws->key_kind = pb->cost_kind; ws->key_d = pb->d; ws->key_ldc = pb->ldc;
@@ -623,7 +625,7 @@ void set_skip(pins_workspace *ws, PassSide &P, int q) {
     P.gam = ptr<float>(ws->sk_gam[q]);
     P.tref = ptr<float>(ws->sk_tref[q]);
     P.qref = ptr<float>(ws->sk_qref[q]);
-    P.skst = ptr<int>(ws->skst) + 8 * q;
+    P.skst = ptr<int>(ws->skst) + 16 * q;
 }
 
 // Fill the pass description of one orientation (0: rows of X, 1: columns).
@@ -1033,7 +1035,9 @@ bool use_tree_cg(pins_workspace *ws, long long m, long long n) {
     }
     // tried by default; a solve that needs > 80 iterations (support far from a
     // spanning tree) sends the next 256 Newton steps to the Jacobi-Schur cluster CG
-    return m + n <= kTreeMaxNodes && ws->nnz <= kTreeNnzMax && ws->csc_ready;
+    long long lim = kTreeNnzMax;
+    if (const char *e2 = getenv("PINS_TREE_NNZ_MAX")) lim = atoll(e2);   // experiments
+    return m + n <= kTreeMaxNodes && ws->nnz <= lim && ws->csc_ready;
 }
 
 int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const double *rhs, double *x,
@@ -1617,6 +1621,19 @@ static int solve_core(const pins_problem *pb, const pins_params *prm, pins_resul
     res->newton_iters = newton_its;
     res->cg_iters = cg_its;
     res->status = converged ? 0 : 1;
+    if (getenv("PINS_SKIP_STATS") && ws->skipk && ws->skst.p) {   // dev instrumentation
+        int h[64];
+        PINS_CUDA(cudaMemcpyAsync(h, ws->skst.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        PINS_CUDA(cudaStreamSynchronize(st));
+        const char *nm[4] = {"lse-row", "lse-col", "sum-row", "sum-col"};
+        for (int q = 0; q < 4; ++q) {
+            unsigned long long a2, b2;
+            memcpy(&a2, h + 16 * q + 6, 8);
+            memcpy(&b2, h + 16 * q + 8, 8);
+            fprintf(stderr, "chunk skip %s: %llu of %llu tested chunks skipped (%.1f %%)\n", nm[q], a2, b2,
+                    b2 ? 100.0 * (double)a2 / (double)b2 : 0.0);
+        }
+    }
     res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return PINS_OK;
 }

@@ -75,7 +75,7 @@ struct PassSide {
     float *qref;                    // [N]: reference-pass skip-test column values
     int *skst;                      // [0] age (< 0: next pass records), [1] skipped, [2] chunks,
                                     // [3] w_lo of the reference (float bits), [4] best skip fraction (ppm),
-                                    // [5] passes left switched off
+                                    // [5] passes left switched off, [6..9] totals skipped / chunks (u64, stats)
     // potentials: pass-row side (fr + phir), pass-column side (gc + psic)
     const double *fr, *phir, *gc, *psic;
     int m1_row;                     // SUM: the "-1" of Eq. (7) sits on the pass-row potential
@@ -525,6 +525,8 @@ __device__ __forceinline__ void skip_switch(const PassSide &P, float w_lo) {
         s[0] += 1;
         if (frac < 50000) s[5] = 16;
         else if (4LL * frac < 3LL * s[4] || s[0] > 64) s[0] = -1;
+        atomicAdd(reinterpret_cast<unsigned long long *>(s + 6), (unsigned long long)s[1]);   // totals (stats)
+        atomicAdd(reinterpret_cast<unsigned long long *>(s + 8), (unsigned long long)s[2]);
     }
     s[1] = 0;
     s[2] = 0;
