@@ -151,7 +151,6 @@ struct Buf {
     double ev[kCC];                              // trial factor
     alignas(16) float qs[kCC];                   // fp32 skip-test value: qt rounded up by 2^-20 |qt|
     alignas(16) float ny[kCC];
-    int skip;                                    // whole chunk below every row's threshold
     alignas(16) float y32[PTS32 ? kCC * DP : 4];
     double y64[PTS64 ? kCC * DP : 1];
     alignas(128) unsigned char yh[COST == PC_SQTC ? kCC * 32 : 16];   // UMMA B tile (kCC x 16 fp16)
@@ -189,21 +188,13 @@ struct Pref {
     static constexpr bool PTS64 = COST == PC_SQ64 || COST == PC_L164;
     static constexpr int NY = (PTS32 || PTS64) ? (kCC * DP + kPT - 1) / kPT : 1;
     double g, psi, ev, bv;
-    float ny, qr, gm;                            // owner warp: qref of the lane's column, certificate
+    float ny;
     float y32[PTS32 ? NY : 1];
     double y64[PTS64 ? NY : 1];
     uint2 yh;
     // global -> registers (this thread's share of columns j0 .. j0+nc-1)
     __device__ __forceinline__ void load(const PassSide &P, long long j0, int nc, bool trial, const SkipCtx &sk) {
         const int tid = threadIdx.x;
-        if (sk.kind == 1 && (tid >> 5) == (trial ? 1 : 0)) {
-            const int lane = tid & 31;
-            qr = lane < nc ? __ldg(sk.qref + j0 + lane) : 0.f;
-            if (lane == 0) {
-                const float4 g4 = __ldg(reinterpret_cast<const float4 *>(sk.gcta + ((j0 - sk.jb) / kCC) * 4));
-                gm = fmaxf(fmaxf(g4.x, g4.y), fmaxf(g4.z, g4.w));
-            }
-        }
         if (tid < kCC) {
             const bool ok = tid < nc;
             g = ok ? P.gc[j0 + tid] : 0.0;
@@ -241,23 +232,11 @@ struct Pref {
             }
         }
     }
-    // owner warp (all 32 lanes; lane = column of the chunk): the chunk skip decision,
-    // or in a reference pass the record of the column values
+    // owner warp, reference pass: record the chunk's column values
     __device__ __forceinline__ void decide(Buf<COST, DP> &B, const SkipCtx &sk, float qs, long long j0,
                                            int nc) const {
         const int lane = threadIdx.x & 31;
-        if (sk.kind == 1) {
-            double d = qs == -INFINITY ? -INFINITY : (double)qs - (double)qr;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
-            if (lane == 0) {
-                const double g = (double)gm, lhs = g + d - sk.dthr;
-                B.skip = lhs + 1e-12 * (fabs(g) + fabs(d) + fabs(sk.dthr)) <= 0.0;
-            }
-        } else {
-            if (sk.kind == 2 && sk.wq && lane < nc) sk.qref[j0 + lane] = qs;
-            if (lane == 0) B.skip = 0;
-        }
+        if (sk.kind == 2 && sk.wq && lane < nc) sk.qref[j0 + lane] = qs;
     }
     // registers -> shared buffer.  qmode: 0 q = (g+psi)/eta, 1 q = (g+psi)/eta - 1
     __device__ __forceinline__ void store(Buf<COST, DP> &B, const PassSide &P, long long i0, long long j0, int nc,
@@ -272,7 +251,7 @@ struct Pref {
                 B.qt[tid] = q;
                 B.qs[tid] = qs;
                 decide(B, sk, qs, j0, nc);
-            } else if (tid == 0) B.skip = 0;
+            }
         } else if (tid < 2 * kCC && trial) {
             B.ev[tid - kCC] = ev;
         }
@@ -426,6 +405,46 @@ using TcFor = typename std::conditional<COST == PC_SQTC, TcState, TcStateT<16>>:
 // Streams the column range [jb, je) through the staging buffers and calls
 // body(c0, nc, buf, dots) per chunk: for PC_SQTC `dots` holds this thread's
 // kCC dot products x_i.y_j from TMEM; for the other costs it is unused.
+// Certificate test of every chunk of the CTA's column range at once (kind 1):
+// warp w tests chunks w, w+4, ...; lane = column.  Sets bit c of bm for each
+// chunk c that is skipped; returns the number skipped (valid in thread 0).
+constexpr int kSkipWords = 256;     // chunk bitmap capacity: 8192 chunks per CTA
+__device__ __forceinline__ int precheck_chunks(const PassSide &P, const SkipCtx &sk, long long jb, long long je,
+                                               long long nch, double inv_eta, int qmode, bool trial,
+                                               unsigned *bm) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nw = (int)((nch + 31) >> 5);
+    for (int t = tid; t < nw; t += kPT) bm[t] = 0u;
+    __syncthreads();
+    for (long long c = warp; c < nch; c += kPT / 32) {
+        const long long j = jb + c * kCC + lane;
+        double d = -INFINITY;
+        if (j < je) {
+            double q = qmode ? pot_p(P.gc[j], P.psic[j], inv_eta) : pot_q(P.gc[j], P.psic[j], inv_eta);
+            if (trial) q = q + P.bv[j];                 // the trial skip-test value (store_trial_qt)
+            const float qs = qs_of(q);
+            if (qs != -INFINITY) d = (double)qs - (double)__ldg(sk.qref + j);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+        if (lane == 0) {
+            const float4 g4 = __ldg(reinterpret_cast<const float4 *>(sk.gcta + c * 4));
+            const double g = (double)fmaxf(fmaxf(g4.x, g4.y), fmaxf(g4.z, g4.w));
+            const double lhs = g + d - sk.dthr;
+            if (lhs + 1e-12 * (fabs(g) + fabs(d) + fabs(sk.dthr)) <= 0.0) atomicOr(bm + (c >> 5), 1u << (c & 31));
+        }
+    }
+    __syncthreads();
+    int n = 0;
+    if (tid == 0)
+        for (int t = 0; t < nw; ++t) n += __popc(bm[t]);
+    return n;
+}
+
+// Streams the kept chunks of the column range [jb, je) through the staging
+// buffers and calls body(c0, nc, buf, dots) per chunk: for PC_SQTC `dots` holds
+// this thread's kCC dot products x_i.y_j from TMEM; for the other costs it is
+// unused.  Returns the number of chunks skipped by certificates (thread 0).
 template <int COST, int DP, class TS, class Body>
 __device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, long long jb, long long je,
                                               double inv_eta, int qmode, bool trial, Buf<COST, DP> *bufs,
@@ -433,62 +452,87 @@ __device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, l
     constexpr int NB = kNBuf<COST>;
     const long long nch = (je - jb + kCC - 1) / kCC;
     if (nch <= 0) return 0;
-    int nskip = 0;
     const int tid = threadIdx.x, warp = tid >> 5;
     Pref<COST, DP> pf;
     constexpr uint32_t idesc = tc::make_idesc(kCC);
     auto nc_of = [&](long long c) { return (int)min((long long)kCC, je - (jb + c * kCC)); };
-    // MMAs are issued only for chunks that are not skipped; the parity of each
-    // buffer's mbarrier advances once per issued MMA
+    __shared__ unsigned bm[kSkipWords];
+    const bool pre = NB > 1 && sk.kind == 1 && nch <= 32LL * kSkipWords;
+    int nskip = 0;
+    if (pre) nskip = precheck_chunks(P, sk, jb, je, nch, inv_eta, qmode, trial, bm);
+    // next kept chunk after c (nch: none)
+    auto next_of = [&](long long c) -> long long {
+        long long t = c + 1;
+        if (!pre) return t;
+        while (t < nch) {
+            const unsigned wv = ~bm[t >> 5] >> (t & 31);
+            if (wv) return min(nch, t + __ffs(wv) - 1);
+            t = (t | 31) + 1;
+        }
+        return nch;
+    };
+    long long cur = next_of(-1);
+    if (cur >= nch) return nskip;
+    long long nxt = next_of(cur);
     uint32_t par = 0u;                               // bit b: parity of buffer b's next phase
-    // prologue: chunk 0 into buffer 0, prefetch chunk 1
-    pf.load(P, jb, nc_of(0), trial, sk);
-    pf.store(bufs[0], P, i0, jb, nc_of(0), inv_eta, qmode, trial, sk);
-    if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0], sk, jb, nc_of(0)); }
-    if (NB > 1 && nch > 1) pf.load(P, jb + kCC, nc_of(1), trial, sk);
+    // prologue: the first chunk into buffer 0, prefetch the next
+    pf.load(P, jb + cur * kCC, nc_of(cur), trial, sk);
+    pf.store(bufs[0], P, i0, jb + cur * kCC, nc_of(cur), inv_eta, qmode, trial, sk);
+    if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0], sk, jb + cur * kCC, nc_of(cur)); }
+    if (NB > 1 && nxt < nch) pf.load(P, jb + nxt * kCC, nc_of(nxt), trial, sk);
     if constexpr (COST == PC_SQTC) tc::fence_proxy_async();
     __syncthreads();
     if constexpr (COST == PC_SQTC) {
-        if (tid == 0 && !bufs[0].skip) {
+        if (tid == 0) {
             tc::fence_after();
             tc::mma_f16(tcs->tbase, tc::make_desc(tcs->ah), tc::make_desc(bufs[0].yh), idesc);
             tc::commit(&tcs->mbar[0]);
         }
     }
-    for (long long c = 0; c < nch; ++c) {
-        const int cur = NB > 1 ? (int)(c & 1) : 0;
-        if (NB > 1 && c + 1 < nch) {
-            const int nxt = cur ^ 1;
-            if constexpr (COST == PC_SQTC) tc::fence_before();
-            __syncthreads();                         // chunk c-1 fully consumed
-            pf.store(bufs[nxt], P, i0, jb + (c + 1) * kCC, nc_of(c + 1), inv_eta, qmode, trial, sk);
-            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[nxt], sk, jb + (c + 1) * kCC, nc_of(c + 1)); }
-            if (c + 2 < nch) pf.load(P, jb + (c + 2) * kCC, nc_of(c + 2), trial, sk);
-            if constexpr (COST == PC_SQTC) tc::fence_proxy_async();
-            __syncthreads();
-            if constexpr (COST == PC_SQTC) {
-                if (tid == 0 && !bufs[nxt].skip) {
-                    tc::fence_after();
-                    tc::mma_f16(tcs->tbase + nxt * kCC, tc::make_desc(tcs->ah), tc::make_desc(bufs[nxt].yh), idesc);
-                    tc::commit(&tcs->mbar[nxt]);
+    int b = 0;
+    const long long first = cur;
+    while (cur < nch) {
+        long long nxt2 = nch;
+        if (NB > 1) {
+            if (nxt < nch) {
+                const int nb = b ^ 1;
+                if constexpr (COST == PC_SQTC) tc::fence_before();
+                __syncthreads();                         // the previous chunk fully consumed
+                pf.store(bufs[nb], P, i0, jb + nxt * kCC, nc_of(nxt), inv_eta, qmode, trial, sk);
+                if (trial) { __syncthreads(); pf.store_trial_qt(bufs[nb], sk, jb + nxt * kCC, nc_of(nxt)); }
+                nxt2 = next_of(nxt);
+                if (nxt2 < nch) pf.load(P, jb + nxt2 * kCC, nc_of(nxt2), trial, sk);
+                if constexpr (COST == PC_SQTC) tc::fence_proxy_async();
+                __syncthreads();
+                if constexpr (COST == PC_SQTC) {
+                    if (tid == 0) {
+                        tc::fence_after();
+                        tc::mma_f16(tcs->tbase + nb * kCC, tc::make_desc(tcs->ah), tc::make_desc(bufs[nb].yh), idesc);
+                        tc::commit(&tcs->mbar[nb]);
+                    }
                 }
             }
-        } else if (NB == 1 && c > 0) {
-            __syncthreads();
-            pf.load(P, jb + c * kCC, nc_of(c), trial, sk);
-            pf.store(bufs[0], P, i0, jb + c * kCC, nc_of(c), inv_eta, qmode, trial, sk);
-            if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0], sk, jb + c * kCC, nc_of(c)); }
-            __syncthreads();
+        } else {
+            if (cur != first) {                          // single buffer (never skipped): sequential chunks
+                __syncthreads();
+                pf.load(P, jb + cur * kCC, nc_of(cur), trial, sk);
+                pf.store(bufs[0], P, i0, jb + cur * kCC, nc_of(cur), inv_eta, qmode, trial, sk);
+                if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0], sk, jb + cur * kCC, nc_of(cur)); }
+                __syncthreads();
+            }
+            nxt2 = nxt + 1;
         }
-        if (bufs[cur].skip) { ++nskip; continue; }   // read before the next chunk boundary's barrier
         float dots[COST == PC_SQTC ? kCC : 1];
         if constexpr (COST == PC_SQTC) {
-            tc::mbar_wait(&tcs->mbar[cur], (par >> cur) & 1u);
-            par ^= 1u << cur;
+            tc::mbar_wait(&tcs->mbar[b], (par >> b) & 1u);
+            par ^= 1u << b;
             tc::fence_after();
-            tc::ld32(tcs->tbase + ((uint32_t)(32 * (warp & 3)) << 16) + cur * kCC, dots);
+            tc::ld32(tcs->tbase + ((uint32_t)(32 * (warp & 3)) << 16) + b * kCC, dots);
         }
-        body(jb + c * kCC, nc_of(c), bufs[cur], dots);
+        body(jb + cur * kCC, nc_of(cur), bufs[b], dots);
+        cur = nxt;
+        nxt = nxt2;
+        if (NB > 1) b ^= 1;
     }
     return nskip;
 }
