@@ -173,6 +173,8 @@ struct pins_workspace {
     const int *tree_rstart = nullptr, *tree_ctr = nullptr;
     const double *tree_frec = nullptr;
     bool csr_ready = false, csc_ready = false;
+    bool x0_enable = false;    // solve_core: warm-start the cluster tree-PCG from the previous direction
+    bool dir_valid = false;    // ws->dir holds the previous Newton system's solution
     double *h = nullptr;   // pinned host scalars (64)
 };
 
@@ -1176,6 +1178,7 @@ int run_cg_tree_cluster(pins_workspace *ws, long long m, long long n, double mu,
     const size_t base = sizeof(double) * (size_t)N;
     const size_t budget = 220 * 1024;
     A.tail_cap = base < budget ? (int)((budget - base) / 40) : 0;
+    A.use_x0 = ws->x0_enable && ws->dir_valid && x == ptr<double>(ws->dir) && getenv("PINS_NO_X0") == nullptr;
     const size_t smem = std::max<size_t>(base + (size_t)A.tail_cap * 40, sizeof(double) * 5 * (size_t)A.R);
     static size_t configured = 0;
     if (smem > configured) {
@@ -1238,6 +1241,7 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
     PINS_CUDA(cudaMemcpyAsync(ws->h + 16, ws->cgst.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
     PINS_CUDA(cudaStreamSynchronize(st));
     const double cg_its = ws->h[16], relres = ws->h[17], slope = ws->h[18], ad = ws->h[19];
+    ws->dir_valid = d == ptr<double>(ws->dir) && relres == relres;
     // algorithmic bytes of this CG launch: per iteration the CSR + CSC (12 B per
     // entry each) and ~10 vector streams of m + n doubles
     g_prof.work[PINS_PROF_CG] += cg_its * (24.0 * (double)ws->nnz + 80.0 * (double)N);
@@ -1509,6 +1513,7 @@ static int solve_core(const pins_problem *pb, const pins_params *prm, pins_resul
     cudaStream_t st = (cudaStream_t)stream;
     pins_workspace *ws = nullptr;
     PINS_TRY(pins_workspace_create(&ws));
+    ws->x0_enable = true;
     struct Guard {
         pins_workspace *w;
         ~Guard() { pins_workspace_destroy(w); }

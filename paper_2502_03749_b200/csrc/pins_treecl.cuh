@@ -44,6 +44,8 @@ struct TreeCLArgs {
     const int *ctr;                      // [1] rounds
     int R;                               // unknowns per worker
     int tail_cap;                        // factor records cached in CTA 0's shared memory
+    int use_x0;                          // 1: start from alpha x (x = the previous system's solution),
+                                         //    alpha = <x,b>/<x,Mx> (the A-norm-optimal multiple)
 };
 
 // y = M p for one worker's slice (p gathered from the owners through DSMEM).
@@ -201,23 +203,67 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
         }
     };
 
-    // ---- init: x = 0, r = b, z = M_T^-1 r, p = z ----
-    double l_bb = 0.0;
-    for (int k = tid; k < nloc; k += kCGT) {
-        const int node = k0 + k;
-        const double bk = A.rhs[node];
-        xs[k] = 0.0;
-        rsl[k] = bk;
-        dg[k] = (node < m ? A.dr[node] : A.dc[node - m]) + mu;
-        vs0[node] = bk;
-        l_bb = fma(bk, bk, l_bb);
-    }
+    // ---- init: x = x0, r = b - M x0, z = M_T^-1 r, p = z ----
     double o1[1];
-    {
-        const double in1[1] = {l_bb};
-        cluster_sums<1>(cl, in1, wsum, redA, bc, o1);      // also: vs0 complete
+    double bb, rr0;
+    if (A.use_x0) {
+        // x0 = alpha xp, xp = the previous Newton system's solution (still in A.x)
+        for (int k = tid; k < nloc; k += kCGT) {
+            const int node = k0 + k;
+            dg[k] = (node < m ? A.dr[node] : A.dc[node - m]) + mu;
+            ps[k] = A.x[node];
+        }
+        cl.sync();                                           // xp slices complete everywhere
+        if (worker)
+            treecl_spmv(cl, A, k0, nloc, ps, [&](int k, double s) { qs[k] = fma(dg[k], ps[k], s); });
+        __syncthreads();
+        double l_pq = 0.0, l_pb = 0.0;
+        for (int k = tid; k < nloc; k += kCGT) {
+            l_pq = fma(ps[k], qs[k], l_pq);
+            l_pb = fma(ps[k], A.rhs[k0 + k], l_pb);
+        }
+        double o2i[2];
+        {
+            const double in2[2] = {l_pq, l_pb};
+            cluster_sums<2>(cl, in2, wsum, redB, bc, o2i);
+        }
+        const double alpha0 = o2i[0] > 0.0 ? o2i[1] / o2i[0] : 0.0;
+        double l_bb = 0.0, l_rr = 0.0;
+        for (int k = tid; k < nloc; k += kCGT) {
+            const int node = k0 + k;
+            const double bk = A.rhs[node];
+            xs[k] = alpha0 * ps[k];
+            const double rv = fma(-alpha0, qs[k], bk);
+            rsl[k] = rv;
+            vs0[node] = rv;
+            l_bb = fma(bk, bk, l_bb);
+            l_rr = fma(rv, rv, l_rr);
+        }
+        double o2r[2];
+        {
+            const double in2[2] = {l_bb, l_rr};
+            cluster_sums<2>(cl, in2, wsum, redA, bc, o2r);  // also: vs0 complete
+        }
+        bb = o2r[0];
+        rr0 = o2r[1];
+    } else {
+        double l_bb = 0.0;
+        for (int k = tid; k < nloc; k += kCGT) {
+            const int node = k0 + k;
+            const double bk = A.rhs[node];
+            xs[k] = 0.0;
+            rsl[k] = bk;
+            dg[k] = (node < m ? A.dr[node] : A.dc[node - m]) + mu;
+            vs0[node] = bk;
+            l_bb = fma(bk, bk, l_bb);
+        }
+        {
+            const double in1[1] = {l_bb};
+            cluster_sums<1>(cl, in1, wsum, redA, bc, o1);      // also: vs0 complete
+        }
+        bb = o1[0];
+        rr0 = bb;
     }
-    const double bb = o1[0];
     if (!worker && bb > 0.0) tree_apply();
     cl.sync();
     double l_rz = 0.0;
@@ -231,7 +277,7 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
         cluster_sums<1>(cl, in1, wsum, redB, bc, o1);
     }
     double rz = o1[0];
-    double rr2 = bb, relres = bb > 0.0 ? 1.0 : 0.0;
+    double rr2 = rr0, relres = bb > 0.0 ? sqrt(rr0 / bb) : 0.0;
     int it = 0;
     while (bb > 0.0 && relres > A.rtol && it < A.maxit) {
         cl.sync();                                           // p complete everywhere
