@@ -729,7 +729,7 @@ __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSid
 // the starting iterate (pass-row side), st[1] = max |f_new - f_old|.
 // =========================================================================
 template <int COST, int DP>
-__global__ void __launch_bounds__(kPT) lse_pass_kernel(PassArgs A) {
+__global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A) {
     __shared__ Buf<COST, DP> bufs[kNBuf<COST>];
     __shared__ TcFor<COST> tcs_storage[1];
     __shared__ float dscr[COST == PC_SQTC ? kPT * (kCC + 1) : 1];
