@@ -193,10 +193,16 @@ typedef struct pins_result {
  * back, so every output is in the caller's order.  The Newton systems use the
  * spanning-tree preconditioned CG when m + n <= 26000 and nnz <= 4e5 (falling
  * back to the Jacobi-Schur cluster CG after a slow tree solve), else Jacobi CG
- * on the whole GPU.  Development knobs (environment):
- * PINS_CG = tree | treecl | cluster | grid forces a solver, PINS_NO_TC=1 turns
- * the tensor-core cross term off, PINS_NO_REORDER=1 the Morton permutation,
- * PINS_TRACE=<file> writes one line per outer iteration.                     */
+ * on the whole GPU; the cluster tree-PCG starts from the
+ * A-norm-optimal multiple of the previous Newton direction.  Dense passes over
+ * integer point clouds skip 32-column chunks that a drift certificate proves
+ * empty (bit-identical results).  Development knobs
+ * (environment): PINS_CG = tree | treecl | cluster | grid forces a solver,
+ * PINS_NO_TC=1 turns the tensor-core cross term off, PINS_NO_REORDER=1 the
+ * Morton permutation, PINS_NO_TILESKIP=1 chunk skipping, PINS_NO_X0=1 the PCG
+ * warm start; PINS_TREE_NNZ_MAX=<n> moves the tree-PCG nnz cap;
+ * PINS_TRACE=<file> writes one line per outer iteration, PINS_SKIP_STATS=1
+ * prints chunk-skip totals to stderr.                                        */
 int pins_solve(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream);
 
 /* End-to-end solve from HOST memory (bench.py's e2e leg): pb_host is a
