@@ -87,7 +87,10 @@ typedef struct pins_params {
 
 void pins_default_params(pins_params *p);
 
-/* Opaque scratch owner (row buffers, CSR/CSC, column partials, CG vectors). */
+/* Opaque scratch owner (row buffers, CSR/CSC, column partials, CG vectors).
+ * Every entry point that takes a pins_problem rebuilds the workspace's
+ * derived problem data (padded point copies, exactness decision, chunk-skip
+ * certificates) at entry, so one workspace may serve many problems.       */
 typedef struct pins_workspace pins_workspace;
 int pins_workspace_create(pins_workspace **ws);
 void pins_workspace_destroy(pins_workspace *ws);
@@ -108,16 +111,29 @@ int pins_center_update(const pins_problem *pb, double *phi, double *psi, double 
 /* One log-domain Sinkhorn sweep in place, Alg. 2 lines 5-6:
  *   f <- eta(log a + 1) - eta LSE_j((g_j - C^k_ij)/eta)
  *   g <- eta(log b + 1) - eta LSE_i((f_i - C^k_ij)/eta)   (with the new f).
- * Fused row-then-column kernel + column finalize.  Asynchronous.             */
+ * Two launches of the half-sweep kernel (row orientation, then column
+ * orientation with the new f); each merges its column splits in its own
+ * last-arriving CTA (no host round trip).  Asynchronous.                     */
 int pins_sinkhorn_sweep(pins_workspace *ws, const pins_problem *pb, const double *phi,
                         const double *psi, double s, double *f, double *g, void *stream);
 
+/* The Sinkhorn phase of Alg. 2 (lines 4-8): sweeps of
+ * pins_sinkhorn_sweep until ||grad P^k||_1 <= tol or max_sweeps sweeps; stops
+ * at exactly the first iterate whose residual is <= tol (the test runs on
+ * the device; batches of sweeps are queued without host round trips).
+ * *sweeps_host = sweeps done, *res_host = final ||grad P^k||_1.  Synchronises. */
+int pins_sinkhorn(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi,
+                  double s, double *f, double *g, double tol, int32_t max_sweeps, int32_t *sweeps_host,
+                  double *res_host, void *stream);
+
 /* Evaluation pass at (f, g): plan X~ of Eq. (7), its row sums r (m) and column
  * sums c (n) (either may be NULL), the gradient norm and objectives.  Host
- * scalars (synchronises):  out_host[0] = ||a - r||_1 + ||b - c||_1 (= ||grad
- * P^k||_1, Eq. (9)),  [1] = sum X~,  [2] = <C, X~>,  [3] = P^k(f,g) (Eq. (8)).
- * If tau > 0 the plan block is also sparsified (X~_ij >= tau) into the
- * workspace CSR, and out_host[4] = nnz.                                       */
+ * scalars (synchronises); out_host must hold at least 6 doubles:
+ * out_host[0] = ||a - r||_1 + ||b - c||_1 (= ||grad P^k||_1, Eq. (9)),
+ * [1] = sum X~,  [2] = <C, X~>,  [3] = P^k(f,g) (Eq. (8)),  [4] = nnz of the
+ * sparsified block (0 if tau == 0),  [5] = max_ij z_ij, z = log X~ (over the
+ * entries the pass evaluates).  If tau > 0 the plan block is also sparsified
+ * (X~_ij >= tau) into the workspace CSR (and CSC).                           */
 int pins_evaluate(pins_workspace *ws, const pins_problem *pb, const double *phi,
                   const double *psi, double s, const double *f, const double *g,
                   double tau, double *r, double *c, double *out_host, void *stream);
@@ -130,9 +146,14 @@ int pins_evaluate(pins_workspace *ws, const pins_problem *pb, const double *phi,
 int pins_get_csr(pins_workspace *ws, int64_t *rowptr, int32_t *colidx, double *val, int64_t cap,
                  int64_t *nnz_host, int64_t *m_host);
 
-/* Sparsify a caller-given dense plan block P (device m x n, leading dim ldp)
- * with the same compaction kernel: CSR of P_ij >= tau (PAPER.md:255-256,
- * reading R3).  Output as pins_get_csr.  Synchronises.                       */
+/* Sparsify a caller-given dense plan block P (device m x n, leading dim ldp):
+ * CSR of P_ij >= tau (reading R3), columns ascending, values
+ * copied bitwise.  Warp-ballot compaction (sparsify_*_kernel), separate from
+ * the evaluation pass's fused compaction (which sparsifies X~(f, g) without
+ * materialising it; see pins_evaluate).  *nnz_host always receives nnz; if
+ * rowptr (m+1, int64), colidx (int32), val (fp64) are non-NULL they receive
+ * the CSR (cap >= nnz required, else PINS_ERR_ARG).  Invalidates the
+ * workspace CSR of the last evaluation.  Synchronises.                      */
 int pins_sparsify_dense(pins_workspace *ws, int64_t m, int64_t n, const double *P, int64_t ldp,
                         double tau, int64_t *rowptr, int32_t *colidx, double *val, int64_t cap,
                         int64_t *nnz_host, void *stream);
@@ -204,6 +225,12 @@ typedef struct pins_result {
  * PINS_TRACE=<file> writes one line per outer iteration, PINS_SKIP_STATS=1
  * prints chunk-skip totals to stderr.                                        */
 int pins_solve(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream);
+
+/* pins_solve on a caller-owned workspace (reused across solves: no per-solve
+ * workspace creation, pinned-buffer allocation or scratch growth).  The
+ * workspace's derived problem data are rebuilt at entry.  Synchronises.     */
+int pins_solve_ws(pins_workspace *ws, const pins_problem *pb, const pins_params *prm, pins_result *res,
+                  void *stream);
 
 /* End-to-end solve from HOST memory (bench.py's e2e leg): pb_host is a
  * pins_problem whose C / x / y / a / b point to HOST memory (pinned for the

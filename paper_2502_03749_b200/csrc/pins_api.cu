@@ -120,9 +120,16 @@ extern "C" int pins_prof_read(int32_t cls, int64_t *launches, double *ms) {
 
 namespace {
 
+// Device buffer owned by its holder (freed by the destructor; not copyable).
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
 };
 
 int ensure(DevBuf &b, size_t bytes) {
@@ -150,7 +157,7 @@ struct SideBufs {
 };
 
 struct pins_workspace {
-    DevBuf colpart, blk, rowsum, gradf, colsum, gradg, rowcnt, rb_col, rb_val;
+    DevBuf rowsum, gradf, colsum, gradg, rowcnt;
     DevBuf rowptr, colidx, val, colcnt, colptr, cursor, rowidx, valT;
     DevBuf cgvec, cgpart, cgst, st, ft, gt, eu, ev, bu, bv, dir, rhs, tab, fsave, gsave, uv;
     DevBuf tr_i, tr_d, tr_u8, tr_u64;   // tree-CG workspace (int / double / byte / u64 pools)
@@ -165,8 +172,8 @@ struct pins_workspace {
     int cost_row = 0, cost_col = 0, dp = 4, skipk = 0;
     int S[2] = {1, 1};
     long long pcap = 16;       // per (row, split) sparsify capacity
-    long long m = 0, n = 0, cap = 64, nnz = 0;
-    int G = 0, nsm = 0, dev = -1;
+    long long m = 0, n = 0, nnz = 0;
+    int nsm = 0, dev = -1;
     bool tree_valid = false;
     long long tree_N = -1;
     int tree_last_its = 0, tree_backoff = 0;
@@ -218,24 +225,8 @@ extern "C" int pins_workspace_create(pins_workspace **out) {
 
 extern "C" void pins_workspace_destroy(pins_workspace *ws) {
     if (!ws) return;
-    DevBuf *bufs[] = {&ws->colpart, &ws->blk, &ws->rowsum, &ws->gradf, &ws->colsum, &ws->gradg,
-                      &ws->rowcnt, &ws->rb_col, &ws->rb_val, &ws->rowptr, &ws->colidx, &ws->val,
-                      &ws->colcnt, &ws->colptr, &ws->cursor, &ws->rowidx, &ws->valT, &ws->cgvec,
-                      &ws->cgpart, &ws->cgst, &ws->st, &ws->ft, &ws->gt, &ws->eu, &ws->ev,
-                      &ws->dir, &ws->rhs, &ws->tab, &ws->fsave, &ws->gsave, &ws->uv, &ws->bu, &ws->bv,
-                      &ws->x32, &ws->y32, &ws->x64, &ws->y64, &ws->nx32, &ws->ny32, &ws->xh, &ws->yh, &ws->pinfo,
-                      &ws->ctl, &ws->gticket, &ws->pst, &ws->tol,
-                      &ws->tr_i, &ws->tr_d, &ws->tr_u8, &ws->tr_u64, &ws->xprev, &ws->xsave};
-    for (DevBuf *b : bufs)
-        if (b->p) cudaFree(b->p);
-    for (int q = 0; q < 2; ++q) {
-        SideBufs &B = ws->sb[q];
-        DevBuf *sbufs[] = {&B.pa, &B.pb, &B.pj, &B.psc, &B.blk, &B.blkoff, &B.ticket, &B.cnt, &B.bcol, &B.bval, &B.jstar};
-        for (DevBuf *b : sbufs)
-            if (b->p) cudaFree(b->p);
-    }
     if (ws->h) cudaFreeHost(ws->h);
-    delete ws;
+    delete ws;   // every DevBuf member frees its device memory
 }
 
 namespace {
@@ -264,84 +255,15 @@ CostDesc make_cd(const pins_problem *pb) {
     cd.ldc = pb->ldc;
     cd.x = pb->x;
     cd.y = pb->y;
-    cd.vec2 = (pb->cost_kind == PINS_COST_DENSE || pb->cost_kind == 3) &&
-              ((reinterpret_cast<uintptr_t>(pb->C) & 15) == 0) && (pb->ldc % 2 == 0);
     return cd;
 }
 
 int dmax_for(int d) { return d <= 2 ? 2 : d <= 3 ? 3 : d <= 10 ? 10 : 16; }
 
-template <bool SP, bool TR>
-cudaError_t launch_eval_t(int kind, int d, int G, cudaStream_t st, const EvalArgs &A) {
-    dim3 grid(G), block(kThreads);
-    const int dm = dmax_for(d);
-    if (kind == 0) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<0, 0, SP, TR><<<grid, block, 0, st>>>(A));
-    else if (kind == 3) {
-        if constexpr (SP && !TR) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<3, 0, true, false><<<grid, block, 0, st>>>(A));
-    } else if (kind == 1) {
-        if (dm == 2) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<1, 2, SP, TR><<<grid, block, 0, st>>>(A));
-        else if (dm == 3) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<1, 3, SP, TR><<<grid, block, 0, st>>>(A));
-        else if (dm == 10) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<1, 10, SP, TR><<<grid, block, 0, st>>>(A));
-        else LAUNCH(PINS_PROF_EVAL, st, eval_kernel<1, 16, SP, TR><<<grid, block, 0, st>>>(A));
-    } else {
-        if (dm == 2) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<2, 2, SP, TR><<<grid, block, 0, st>>>(A));
-        else if (dm == 3) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<2, 3, SP, TR><<<grid, block, 0, st>>>(A));
-        else if (dm == 10) LAUNCH(PINS_PROF_EVAL, st, eval_kernel<2, 10, SP, TR><<<grid, block, 0, st>>>(A));
-        else LAUNCH(PINS_PROF_EVAL, st, eval_kernel<2, 16, SP, TR><<<grid, block, 0, st>>>(A));
-    }
-    return cudaGetLastError();
-}
-
-cudaError_t launch_eval(bool sp, bool tr, int kind, int d, int G, cudaStream_t st, const EvalArgs &A) {
-    if (sp && tr) return launch_eval_t<true, true>(kind, d, G, st, A);
-    if (sp) return launch_eval_t<true, false>(kind, d, G, st, A);
-    if (tr) return launch_eval_t<false, true>(kind, d, G, st, A);
-    return launch_eval_t<false, false>(kind, d, G, st, A);
-}
-
-template <template <int, int> class K>
-struct Dummy {};
-
-cudaError_t launch_sweep(int kind, int d, long long m, long long n, cudaStream_t st, int nsm,
-                         const SweepArgs &A) {
-    const int dm = dmax_for(d);
-    const int rows_blocks = (int)std::min<long long>((m + kWarps - 1) / kWarps, (long long)nsm * 16);
-    const int col_blocks = (int)std::min<long long>((n + 31) / 32, (long long)nsm * 8);
-#define SWEEP_PAIR(KD, DM)                                                  \
-    do {                                                                    \
-        LAUNCH(PINS_PROF_SWEEP_ROW, st, sweep_row_kernel<KD, DM><<<rows_blocks, kThreads, 0, st>>>(A));     \
-        LAUNCH(PINS_PROF_SWEEP_COL, st, sweep_col_kernel<KD, DM><<<col_blocks, kThreads, 0, st>>>(A));      \
-    } while (0)
-    if (kind == 0) SWEEP_PAIR(0, 0);
-    else if (kind == 1) {
-        if (dm == 2) SWEEP_PAIR(1, 2);
-        else if (dm == 3) SWEEP_PAIR(1, 3);
-        else if (dm == 10) SWEEP_PAIR(1, 10);
-        else SWEEP_PAIR(1, 16);
-    } else {
-        if (dm == 2) SWEEP_PAIR(2, 2);
-        else if (dm == 3) SWEEP_PAIR(2, 3);
-        else if (dm == 10) SWEEP_PAIR(2, 10);
-        else SWEEP_PAIR(2, 16);
-    }
-#undef SWEEP_PAIR
-    return cudaGetLastError();
-}
-
 int grid_1d(long long work, int nsm, int per_sm = 8) {
     long long g = (work + 255) / 256;
     if (g < 1) g = 1;
     return (int)std::min<long long>(g, (long long)nsm * per_sm);
-}
-
-// choose the eval grid: balanced row ranges, <= kRMax rows per CTA
-int eval_grid(long long m, int nsm) {
-    const long long slots = (long long)nsm * 2;
-    long long waves = (m + kRMax * slots - 1) / (kRMax * slots);
-    long long G = slots * std::max<long long>(waves, 1);
-    G = std::min(G, m);
-    G = std::max(G, (m + kRMax - 1) / kRMax);
-    return (int)G;
 }
 
 int prepare(pins_workspace *ws, const pins_problem *pb) {
@@ -351,15 +273,11 @@ int prepare(pins_workspace *ws, const pins_problem *pb) {
         ws->n = n;
         ws->csr_ready = ws->csc_ready = false;
     }
-    ws->G = eval_grid(m, ws->nsm);
     const long long N = m + n;
-    PINS_TRY(ensure(ws->colpart, sizeof(double) * ws->G * n));
-    PINS_TRY(ensure(ws->blk, sizeof(double) * ws->G * 4));
     PINS_TRY(ensure(ws->rowsum, sizeof(double) * m));
     PINS_TRY(ensure(ws->gradf, sizeof(double) * m));
     PINS_TRY(ensure(ws->colsum, sizeof(double) * n));
     PINS_TRY(ensure(ws->gradg, sizeof(double) * n));
-    PINS_TRY(ensure(ws->rowcnt, sizeof(int) * m));
     PINS_TRY(ensure(ws->st, sizeof(double) * 32));
     PINS_TRY(ensure(ws->ft, sizeof(double) * m));
     PINS_TRY(ensure(ws->gt, sizeof(double) * n));
@@ -370,8 +288,6 @@ int prepare(pins_workspace *ws, const pins_problem *pb) {
     PINS_TRY(ensure(ws->fsave, sizeof(double) * m));
     PINS_TRY(ensure(ws->gsave, sizeof(double) * n));
     PINS_TRY(ensure(ws->uv, sizeof(double) * N));
-    PINS_TRY(ensure(ws->rb_col, sizeof(int) * m * ws->cap));
-    PINS_TRY(ensure(ws->rb_val, sizeof(double) * m * ws->cap));
     return PINS_OK;
 }
 
@@ -416,96 +332,24 @@ struct EvalOut {
     double gnorm, sumX, cost, dualP, nnz, maxz, maxcnt, em1, maxr, maxc, af;
 };
 
-// Legacy evaluation pass (one CTA per row range, ballot compaction); used
-// only by pins_sparsify_dense, whose "cost" is the caller's plan (KIND 3).
-int run_eval_legacy(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi,
-             double s, const double *f, const double *g, double tau, bool trial,
-             cudaStream_t st, EvalOut *out) {
-    PINS_TRY(prepare(ws, pb));
-    const bool sparse = tau > 0.0;
-    for (int attempt = 0; attempt < 4; ++attempt) {
-        EvalArgs A;
-        A.m = pb->m;
-        A.n = pb->n;
-        A.cd = make_cd(pb);
-        A.f = f;
-        A.phi = phi;
-        A.g = g;
-        A.psi = psi;
-        A.a = pb->a;
-        A.inv_eta = 1.0 / pb->eta;
-        A.w = s * pb->cost_scale / pb->eta;
-        A.tau = tau;
-        A.cap = ws->cap;
-        A.eu = ptr<double>(ws->eu);
-        A.ev = ptr<double>(ws->ev);
-        A.tab = ptr<ExpTable>(ws->tab);
-        A.rowsum = ptr<double>(ws->rowsum);
-        A.gradf = ptr<double>(ws->gradf);
-        A.colpart = ptr<double>(ws->colpart);
-        A.blk = ptr<double>(ws->blk);
-        A.rowcnt = ptr<int>(ws->rowcnt);
-        A.rb_col = ptr<int>(ws->rb_col);
-        A.rb_val = ptr<double>(ws->rb_val);
-        PINS_CUDA(launch_eval(sparse, trial, pb->cost_kind, pb->d, ws->G, st, A));
-        LAUNCH(PINS_PROF_REDUCE, st, colsum_kernel<<<grid_1d(pb->n, ws->nsm), 256, 0, st>>>(
-            pb->n, ws->G, ptr<double>(ws->colpart), pb->b, ptr<double>(ws->colsum), ptr<double>(ws->gradg)));
-        PINS_CUDA(cudaGetLastError());
-        LAUNCH(PINS_PROF_REDUCE, st, stats_kernel<<<1, 1024, 0, st>>>(pb->m, pb->n, ws->G, ptr<double>(ws->gradf),
-                                         ptr<double>(ws->gradg), ptr<double>(ws->rowsum),
-                                         ptr<double>(ws->blk), sparse ? ptr<int>(ws->rowcnt) : nullptr,
-                                         ws->cap, ptr<double>(ws->st)));
-        PINS_CUDA(cudaGetLastError());
-        LAUNCH(PINS_PROF_REDUCE, st, dots_kernel<<<1, 1024, 0, st>>>(pb->m, pb->n, pb->a, f, pb->b, g, ptr<double>(ws->rowsum),
-                                        ptr<double>(ws->colsum), ptr<double>(ws->st)));
-        PINS_CUDA(cudaGetLastError());
-        PINS_CUDA(cudaMemcpyAsync(ws->h, ws->st.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, st));
-        PINS_CUDA(cudaStreamSynchronize(st));
-        const double *h = ws->h;
-        out->gnorm = h[0] + h[1];
-        out->sumX = h[2];
-        out->cost = h[3] * pb->cost_scale;
-        out->em1 = h[4];
-        out->maxz = h[5];
-        out->maxcnt = h[6];
-        out->nnz = h[7];
-        out->af = h[8];
-        out->maxr = h[9];
-        out->maxc = h[10];
-        out->dualP = h[8] - pb->eta * h[2];
-        ws->csr_ready = ws->csc_ready = false;
-        if (!sparse) return PINS_OK;
-        if (out->maxcnt <= (double)ws->cap) {
-            // CSR from the row buffers
-            PINS_TRY(ensure(ws->rowptr, sizeof(long long) * (pb->m + 1)));
-            const long long nnz = (long long)out->nnz;
-            PINS_TRY(ensure(ws->colidx, sizeof(int) * std::max<long long>(nnz, 1)));
-            PINS_TRY(ensure(ws->val, sizeof(double) * std::max<long long>(nnz, 1)));
-            LAUNCH(PINS_PROF_CSR, st, scan_counts_kernel<<<1, 1024, 0, st>>>(pb->m, ptr<int>(ws->rowcnt), ws->cap,
-                                                   ptr<long long>(ws->rowptr)));
-            LAUNCH(PINS_PROF_CSR, st, csr_copy_kernel<<<grid_1d(pb->m * 32, ws->nsm), 256, 0, st>>>(
-                pb->m, ws->cap, ptr<long long>(ws->rowptr), ptr<int>(ws->rb_col),
-                ptr<double>(ws->rb_val), ptr<int>(ws->colidx), ptr<double>(ws->val)));
-            PINS_CUDA(cudaGetLastError());
-            ws->nnz = nnz;
-            ws->csr_ready = true;
-            return PINS_OK;
-        }
-        // overflow: grow the per-row capacity and redo the pass
-        long long c = ws->cap;
-        while ((double)c < out->maxcnt) c *= 2;
-        ws->cap = c;
-        PINS_TRY(ensure(ws->rb_col, sizeof(int) * pb->m * ws->cap));
-        PINS_TRY(ensure(ws->rb_val, sizeof(double) * pb->m * ws->cap));
-    }
-    snprintf(g_err, sizeof g_err, "row buffer capacity did not converge");
-    return PINS_ERR_NUMERIC;
-}
-
-
 // ===================================================================== v2
 // Thread-per-row dense passes (pins_pass.cuh).
 int dp_for(int d) { return d <= 4 ? 4 : d <= 12 ? 12 : 16; }
+
+// Forget the derived cost data of the previous problem.  Every public entry
+// point that takes a pins_problem calls this first, so a workspace reused with
+// a new problem -- even one whose arrays sit at the old addresses, or whose
+// points were updated in place -- never sees stale coordinates, exactness
+// decisions or chunk-skip certificates.  (pins_solve keeps its state across
+// its own internal calls.)
+void invalidate_problem(pins_workspace *ws) {
+    ws->key_C = ws->key_x = ws->key_y = nullptr;
+    ws->key_m = ws->key_n = ws->key_ldc = -1;
+    ws->key_kind = ws->key_d = -1;
+    ws->tree_valid = false;
+    ws->dir_valid = false;
+    ws->tree_backoff = 0;
+}
 
 // (Re)build the derived cost data when the problem identity changes: padded
 // fp32 / fp64 point copies, norms, the exact-fp32 decision, argmax seeds.
@@ -1355,8 +1199,31 @@ extern "C" int pins_sinkhorn_sweep(pins_workspace *ws, const pins_problem *pb, c
                                    const double *psi, double s, double *f, double *g, void *stream) {
     PINS_ARG(ws != nullptr, "ws");
     PINS_TRY(check_problem(pb));
+    invalidate_problem(ws);
     PINS_ARG(phi && psi && f && g && s > 0.0, "phi, psi, f, g, s > 0");
     return do_sweep(ws, pb, phi, psi, s, f, g, (cudaStream_t)stream);
+}
+
+extern "C" int pins_sinkhorn(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi,
+                             double s, double *f, double *g, double tol, int32_t max_sweeps, int32_t *sweeps_host,
+                             double *res_host, void *stream) {
+    PINS_ARG(ws != nullptr && sweeps_host && res_host, "ws, sweeps, res");
+    PINS_TRY(check_problem(pb));
+    invalidate_problem(ws);
+    PINS_ARG(phi && psi && f && g && s > 0.0 && max_sweeps >= 0 && tol >= 0.0, "phi, psi, f, g, s > 0, budget, tol");
+    cudaStream_t st = (cudaStream_t)stream;
+    pins_params prm;
+    pins_default_params(&prm);
+    prm.T1 = max_sweeps;
+    prm.sink_tol = tol;
+    EvalOut e;
+    PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, 0.0, false, st, &e));
+    int t = 0;
+    PINS_TRY(sinkhorn_phase(ws, pb, &prm, phi, psi, s, f, g, e.gnorm, &t, st));
+    if (t > 0) PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, 0.0, false, st, &e));
+    *sweeps_host = t;
+    *res_host = e.gnorm;
+    return PINS_OK;
 }
 
 extern "C" int pins_evaluate(pins_workspace *ws, const pins_problem *pb, const double *phi,
@@ -1364,6 +1231,7 @@ extern "C" int pins_evaluate(pins_workspace *ws, const pins_problem *pb, const d
                              double *r, double *c, double *out_host, void *stream) {
     PINS_ARG(ws != nullptr && out_host != nullptr, "ws, out_host");
     PINS_TRY(check_problem(pb));
+    invalidate_problem(ws);
     PINS_ARG(phi && psi && f && g && s > 0.0, "phi, psi, f, g, s > 0");
     cudaStream_t st = (cudaStream_t)stream;
     EvalOut e;
@@ -1402,21 +1270,33 @@ extern "C" int pins_sparsify_dense(pins_workspace *ws, int64_t m, int64_t n, con
                                    int64_t ldp, double tau, int64_t *rowptr, int32_t *colidx,
                                    double *val, int64_t cap, int64_t *nnz_host, void *stream) {
     PINS_ARG(ws && P && nnz_host && m >= 1 && n >= 1 && ldp >= n && tau > 0.0, "arguments");
+    PINS_ARG(m < (1LL << 31) && n < (1LL << 31), "m, n < 2^31");
     cudaStream_t st = (cudaStream_t)stream;
-    PINS_TRY(ensure(ws->fsave, sizeof(double) * (m + n)));
-    PINS_TRY(ensure(ws->gsave, sizeof(double) * (m + n)));
-    PINS_CUDA(cudaMemsetAsync(ws->fsave.p, 0, sizeof(double) * (m + n), st));
-    PINS_CUDA(cudaMemsetAsync(ws->gsave.p, 0, sizeof(double) * (m + n), st));
-    // a dummy problem whose "cost" is the given plan (kernel KIND 3: X = P)
-    pins_problem pb;
-    memset(&pb, 0, sizeof pb);
-    pb.m = m; pb.n = n; pb.cost_kind = 3; pb.C = P; pb.ldc = ldp; pb.cost_scale = 1.0; pb.eta = 1.0;
-    pb.a = ptr<double>(ws->fsave); pb.b = ptr<double>(ws->fsave) + m;
-    const double *z = ptr<double>(ws->gsave);
-    EvalOut e;
-    PINS_TRY(run_eval_legacy(ws, &pb, z, z + m, 1.0, z, z + m, tau, false, st, &e));
-    int64_t mm = 0;
-    return pins_get_csr(ws, rowptr, colidx, val, cap, nnz_host, &mm);
+    PINS_TRY(ensure(ws->rowcnt, sizeof(int) * m));
+    PINS_TRY(ensure(ws->rowptr, sizeof(long long) * (m + 1)));
+    const int gw = grid_1d(m * 32, ws->nsm);
+    LAUNCH(PINS_PROF_CSR, st, sparsify_count_kernel<<<gw, 256, 0, st>>>(m, n, P, ldp, tau, ptr<int>(ws->rowcnt)));
+    LAUNCH(PINS_PROF_CSR, st, scan_counts_kernel<<<1, 1024, 0, st>>>(m, ptr<int>(ws->rowcnt), 1LL << 40,
+                                                                    ptr<long long>(ws->rowptr)));
+    PINS_CUDA(cudaGetLastError());
+    long long *hn = reinterpret_cast<long long *>(ws->h + 48);
+    PINS_CUDA(cudaMemcpyAsync(hn, ptr<long long>(ws->rowptr) + m, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    PINS_CUDA(cudaStreamSynchronize(st));
+    const long long nnz = *hn;
+    *nnz_host = nnz;
+    // the workspace's rowptr buffer was reused: its evaluation CSR / CSC are stale
+    ws->m = m;
+    ws->nnz = nnz;
+    ws->csc_ready = false;
+    ws->csr_ready = false;
+    if (!(rowptr && colidx && val)) return PINS_OK;
+    PINS_ARG(cap >= nnz, "cap < nnz");
+    LAUNCH(PINS_PROF_CSR, st, sparsify_fill_kernel<<<gw, 256, 0, st>>>(m, n, P, ldp, tau, ptr<long long>(ws->rowptr),
+                                                                      colidx, val));
+    PINS_CUDA(cudaGetLastError());
+    PINS_CUDA(cudaMemcpyAsync(rowptr, ws->rowptr.p, sizeof(long long) * (m + 1), cudaMemcpyDeviceToDevice, st));
+    PINS_CUDA(cudaStreamSynchronize(st));
+    return PINS_OK;
 }
 
 extern "C" int pins_cg(pins_workspace *ws, int64_t m, int64_t n, const int64_t *rowptr,
@@ -1443,6 +1323,7 @@ extern "C" int pins_newton_step(pins_workspace *ws, const pins_problem *pb, cons
                                 double *info_host, void *stream) {
     PINS_ARG(ws && prm && info_host, "ws, prm, info");
     PINS_TRY(check_problem(pb));
+    invalidate_problem(ws);
     PINS_ARG(phi && psi && f && g && s > 0.0, "phi, psi, f, g, s > 0");
     cudaStream_t st = (cudaStream_t)stream;
     const double tau = prm->theta / ((double)pb->m * (double)pb->n);
@@ -1456,6 +1337,7 @@ extern "C" int pins_residuals(pins_workspace *ws, const pins_problem *pb, const 
                               double *v, double *res_host, void *stream) {
     PINS_ARG(ws && res_host, "ws, res");
     PINS_TRY(check_problem(pb));
+    invalidate_problem(ws);
     PINS_ARG(phi && psi && f && g && s > 0.0, "phi, psi, f, g, s > 0");
     cudaStream_t st = (cudaStream_t)stream;
     EvalOut e;
@@ -1499,25 +1381,25 @@ extern "C" int pins_plan(const pins_problem *pb, const double *phi, const double
     const double inv_eta = 1.0 / pb->eta, w = s * pb->cost_scale / pb->eta;
     const int G = grid_1d(pb->m * pb->n, 148, 16);
     if (pb->cost_kind == 0)
-        LAUNCH(PINS_PROF_PLAN, st, plan_kernel<0, 0><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx));
+        LAUNCH(PINS_PROF_PLAN, st, plan_kernel<0><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx));
     else if (pb->cost_kind == 1)
-        LAUNCH(PINS_PROF_PLAN, st, plan_kernel<1, 16><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx));
+        LAUNCH(PINS_PROF_PLAN, st, plan_kernel<1><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx));
     else
-        LAUNCH(PINS_PROF_PLAN, st, plan_kernel<2, 16><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx));
+        LAUNCH(PINS_PROF_PLAN, st, plan_kernel<2><<<G, 256, 0, st>>>(pb->m, pb->n, cd, f, phi, g, psi, inv_eta, w, ptr<ExpTable>(tab), X, ldx));
     PINS_CUDA(cudaGetLastError());
     return PINS_OK;
 }
 
-static int solve_core(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream) {
+static int solve_core(pins_workspace *ws, const pins_problem *pb, const pins_params *prm, pins_result *res,
+                      void *stream) {
     auto t0 = std::chrono::steady_clock::now();
     cudaStream_t st = (cudaStream_t)stream;
-    pins_workspace *ws = nullptr;
-    PINS_TRY(pins_workspace_create(&ws));
+    invalidate_problem(ws);
     ws->x0_enable = true;
-    struct Guard {
+    struct Reset {
         pins_workspace *w;
-        ~Guard() { pins_workspace_destroy(w); }
-    } guard{ws};
+        ~Reset() { w->x0_enable = false; }
+    } reset{ws};
     const long long m = pb->m, n = pb->n;
     double *f = res->f, *g = res->g, *phi = res->phi, *psi = res->psi;
     const double tau = prm->theta / ((double)m * (double)n);
@@ -1715,11 +1597,11 @@ static int morton_order(long long np, int d, const double *pts, const double *lo
     PINS_TRY(ensure(sortmp, tb));
     PINS_CUDA(cub::DeviceRadixSort::SortPairs(sortmp.p, tb, k0, k1, i0, perm, (int)np, 0, 64, st));
     PINS_CUDA(cudaStreamSynchronize(st));
-    cudaFree(sortmp.p);
     return PINS_OK;
 }
 
-extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream) {
+static int solve_entry(pins_workspace *ws, const pins_problem *pb, const pins_params *prm, pins_result *res,
+                       void *stream) {
     PINS_TRY(check_problem(pb));
     PINS_ARG(prm && res && res->f && res->g && res->phi && res->psi, "params / result buffers");
     PINS_ARG(prm->K >= 1 && prm->T2 >= 0 && prm->T1 >= 0, "budgets");
@@ -1729,7 +1611,7 @@ extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_r
     const bool reorder = pb->cost_kind != PINS_COST_DENSE && (double)m * (double)n >= 65536.0 &&
                          getenv("PINS_NO_REORDER") == nullptr;
     if (!reorder) {
-        int rc = solve_core(pb, prm, res, stream);
+        int rc = solve_core(ws, pb, prm, res, stream);
         res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         return rc;
     }
@@ -1742,10 +1624,6 @@ extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_r
     double *xp = ptr<double>(buf), *yp = xp + m * d, *ap = yp + n * d, *bp = ap + m;
     double *o = bp + n;                       // 6 (m+n) result slots
     int *px = reinterpret_cast<int *>(o + 6 * (m + n)), *py = px + m;
-    struct Free {
-        DevBuf *b[3];
-        ~Free() { for (DevBuf *x : b) if (x->p) cudaFree(x->p); }
-    } fr{{&buf, &lohi, &tmp}};
     LAUNCH(PINS_PROF_VEC, st, bbox_kernel<<<1, 1024, 0, st>>>(m, n, d, pb->x, pb->y, ptr<double>(lohi)));
     PINS_CUDA(cudaGetLastError());
     PINS_TRY(morton_order(m, d, pb->x, ptr<double>(lohi), px, tmp, st));
@@ -1759,7 +1637,7 @@ extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_r
     r.f = o; r.g = o + m; r.phi = o + (m + n); r.psi = o + (m + n) + m;
     r.u = res->u ? o + 2 * (m + n) : nullptr;
     r.v = res->v ? o + 2 * (m + n) + m : nullptr;
-    PINS_TRY(solve_core(&q, prm, &r, stream));
+    PINS_TRY(solve_core(ws, &q, prm, &r, stream));
     double *const src[6] = {r.f, r.g, r.phi, r.psi, r.u, r.v};
     double *const dst[6] = {res->f, res->g, res->phi, res->psi, res->u, res->v};
     for (int t = 0; t < 6; ++t) {
@@ -1775,4 +1653,18 @@ extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_r
     res->f = keep[0]; res->g = keep[1]; res->phi = keep[2]; res->psi = keep[3]; res->u = keep[4]; res->v = keep[5];
     res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return PINS_OK;
+}
+
+extern "C" int pins_solve_ws(pins_workspace *ws, const pins_problem *pb, const pins_params *prm, pins_result *res,
+                             void *stream) {
+    PINS_ARG(ws != nullptr, "ws");
+    return solve_entry(ws, pb, prm, res, stream);
+}
+
+extern "C" int pins_solve(const pins_problem *pb, const pins_params *prm, pins_result *res, void *stream) {
+    pins_workspace *ws = nullptr;
+    PINS_TRY(pins_workspace_create(&ws));
+    const int rc = solve_entry(ws, pb, prm, res, stream);
+    pins_workspace_destroy(ws);
+    return rc;
 }

@@ -3,19 +3,15 @@
 //  * pexp():   full-precision fp64 exp, table-driven (2^(j/64) hi/lo table in
 //              shared memory, degree-6 polynomial on |r| <= ln2/128).  ~10
 //              fp64 pipe ops instead of ~20 for the libdevice routine.
-//  * lse_push / lse_merge: online log-sum-exp state (max, scaled sum).
-//  * cost tiles: dense C rows (128-bit loads) or on-the-fly squared
-//              Euclidean / L1 distances from point coordinates.
+//  * CostDesc: the cost source (dense C or point coordinates).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace pins {
 
-constexpr int kThreads = 256;          // 8 warps per CTA
+constexpr int kThreads = 256;          // 8 warps per CTA (CG, vector kernels)
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 2 * kThreads;   // columns per chunk (2 adjacent per thread)
-constexpr int kRMax = 32;              // max rows per CTA in the dense passes
 
 struct ExpTable {
     double hi[64];
@@ -87,25 +83,6 @@ __device__ __forceinline__ void load_exp_table(const ExpTable *__restrict__ g, d
     }
 }
 
-// online log-sum-exp state: value = mx + log(sm)
-__device__ __forceinline__ void lse_push(double &mx, double &sm, double x, const double *thi,
-                                         const double *tlo) {
-    if (x > mx) {
-        sm = sm * pexp(mx - x, thi, tlo) + 1.0;
-        mx = x;
-    } else {
-        sm += pexp(x - mx, thi, tlo);
-    }
-}
-
-__device__ __forceinline__ void lse_merge(double &mx, double &sm, double mx2, double sm2,
-                                          const double *thi, const double *tlo) {
-    double M = fmax(mx, mx2);
-    if (M == -INFINITY) { mx = M; sm = 0.0; return; }
-    sm = sm * pexp(mx - M, thi, tlo) + sm2 * pexp(mx2 - M, thi, tlo);
-    mx = M;
-}
-
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -132,61 +109,6 @@ struct CostDesc {
     long long ldc;
     const double *x;   // m x d
     const double *y;   // n x d
-    int vec2;          // dense: rows 16-byte aligned and ldc even -> 128-bit loads
 };
-
-// Per-thread column coordinates (2 adjacent columns j, j+1).
-template <int KIND, int DMAX>
-struct ColPts {
-    double y0[DMAX > 0 ? DMAX : 1];
-    double y1[DMAX > 0 ? DMAX : 1];
-    __device__ __forceinline__ void load(const CostDesc &cd, long long j, long long n) {
-        if constexpr (KIND == 1 || KIND == 2) {
-#pragma unroll
-            for (int k = 0; k < DMAX; ++k) {
-                y0[k] = (k < cd.d && j < n) ? cd.y[j * cd.d + k] : 0.0;
-                y1[k] = (k < cd.d && j + 1 < n) ? cd.y[(j + 1) * cd.d + k] : 0.0;
-            }
-        }
-    }
-};
-
-// distance of row point xr (shared memory, d values) to the two column points
-template <int KIND, int DMAX>
-__device__ __forceinline__ void pts_dist2(const double *__restrict__ xr, const ColPts<KIND, DMAX> &cp,
-                                          int d, double &D0, double &D1) {
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < DMAX; ++k) {
-        if (k < d) {
-            double xv = xr[k];
-            double t0 = xv - cp.y0[k];
-            double t1 = xv - cp.y1[k];
-            if constexpr (KIND == 1) {
-                s0 = fma(t0, t0, s0);
-                s1 = fma(t1, t1, s1);
-            } else {
-                s0 += fabs(t0);
-                s1 += fabs(t1);
-            }
-        }
-    }
-    D0 = s0;
-    D1 = s1;
-}
-
-// dense: the two entries C[i, j], C[i, j+1] (j even); tail-safe
-__device__ __forceinline__ void dense_load2(const CostDesc &cd, long long i, long long j, long long n,
-                                            double &D0, double &D1) {
-    const double *row = cd.C + i * cd.ldc;
-    if (cd.vec2 && j + 1 < n) {
-        double2 v = __ldg(reinterpret_cast<const double2 *>(row + j));
-        D0 = v.x;
-        D1 = v.y;
-    } else {
-        D0 = (j < n) ? __ldg(row + j) : 0.0;
-        D1 = (j + 1 < n) ? __ldg(row + j + 1) : 0.0;
-    }
-}
 
 }  // namespace pins

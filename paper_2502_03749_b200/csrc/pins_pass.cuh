@@ -1078,30 +1078,6 @@ __global__ void __launch_bounds__(kPT) sum_pass_kernel(PassArgs A) {
     }
 }
 
-// CSR (or CSC) from the per-(row, split) buffers: rowptr from an exclusive
-// scan of min(cnt, cap) over (row, split) in row-major order (done by
-// scan_counts_kernel), then one warp per pass row copies its S segments.
-__global__ void seg_copy_kernel(long long M, int S, long long cap, const long long *segptr,
-                                const int *bcol, const double *bval, long long *rowptr, int *colidx,
-                                double *val) {
-    const int lane = threadIdx.x & 31;
-    const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long i = gw; i < M; i += nw) {
-        if (lane == 0) rowptr[i] = segptr[i * S];
-        if (i == M - 1 && lane == 0) rowptr[M] = segptr[M * S];
-        for (int s = 0; s < S; ++s) {
-            const long long seg = i * S + s;
-            const long long dst = segptr[seg], len = segptr[seg + 1] - dst;
-            const long long src = seg * cap;
-            for (long long k = lane; k < len; k += 32) {
-                colidx[dst + k] = bcol[src + k];
-                val[dst + k] = bval[src + k];
-            }
-        }
-    }
-}
-
 }  // namespace pins
 
 namespace pins {
@@ -1233,6 +1209,38 @@ __global__ void prep_points_kernel(long long np, int d, int dp, const double *x,
         atomicMax(info + 0, (unsigned long long)__double_as_longlong(amax));
         atomicMax(info + 1, (unsigned long long)__double_as_longlong(nmax));
         atomicAdd(info + 2, nonint);
+    }
+}
+
+// Dense plan materialisation X~(f, g) (Eq. (7); pins_plan).  The exponent is
+// formed exactly as in sum_pass_kernel -- z = fma(-w, D, pot_p(f, phi) +
+// pot_q(g, psi)), no FMA contraction of the potentials, D in the same operation
+// order -- and pexp agrees with pexp_lean bit for bit on the pass's clamp range,
+// so every entry the sum pass keeps (X~ >= tau) has the same bits here: the
+// sparsifier's parity test thresholds this plan on the host.
+template <int KIND>
+__global__ void plan_kernel(long long m, long long n, CostDesc cd, const double *f,
+                            const double *phi, const double *g, const double *psi,
+                            double inv_eta, double w, const ExpTable *tab, double *X, long long ldx) {
+    __shared__ double thi[64], tlo[64];
+    load_exp_table(tab, thi, tlo);
+    __syncthreads();
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m * n;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / n, j = e % n;
+        double D;
+        if constexpr (KIND == 0) {
+            D = cd.C[i * cd.ldc + j];
+        } else {
+            double s = 0.0;
+            for (int k = 0; k < cd.d; ++k) {
+                const double t = cd.x[i * cd.d + k] - cd.y[j * cd.d + k];
+                s = (KIND == 1) ? fma(t, t, s) : s + fabs(t);
+            }
+            D = s;
+        }
+        const double z = fma(-w, D, __dadd_rn(pot_p(f[i], phi[i], inv_eta), pot_q(g[j], psi[j], inv_eta)));
+        X[i * ldx + j] = pexp(z, thi, tlo);
     }
 }
 

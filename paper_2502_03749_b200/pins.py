@@ -20,9 +20,10 @@ COST_DENSE, COST_SQEUCLID, COST_L1 = 0, 1, 2
 
 EXPORTS = [
     "pins_default_params", "pins_workspace_create", "pins_workspace_destroy", "pins_last_error",
-    "pins_center_init", "pins_center_update", "pins_sinkhorn_sweep", "pins_evaluate",
+    "pins_center_init", "pins_center_update", "pins_sinkhorn_sweep", "pins_sinkhorn", "pins_evaluate",
     "pins_get_csr", "pins_sparsify_dense", "pins_cg", "pins_newton_step", "pins_residuals", "pins_plan", "pins_solve",
     "pins_prof_enable", "pins_prof_reset", "pins_prof_read", "pins_prof_read_work", "pins_solve_host",
+    "pins_solve_ws",
 ]
 
 
@@ -70,6 +71,7 @@ def load():
         "pins_center_init": (I32, [P, V, V, POINTER(D), V]),
         "pins_center_update": (I32, [P, V, V, POINTER(D), V, V, V]),
         "pins_sinkhorn_sweep": (I32, [V, P, V, V, D, V, V, V]),
+        "pins_sinkhorn": (I32, [V, P, V, V, D, V, V, D, I32, POINTER(I32), POINTER(D), V]),
         "pins_evaluate": (I32, [V, P, V, V, D, V, V, D, V, V, POINTER(D), V]),
         "pins_get_csr": (I32, [V, V, V, V, I64, POINTER(I64), POINTER(I64)]),
         "pins_sparsify_dense": (I32, [V, I64, I64, V, I64, D, V, V, V, I64, POINTER(I64), V]),
@@ -79,6 +81,7 @@ def load():
         "pins_residuals": (I32, [V, P, V, V, D, V, V, V, V, POINTER(D), V]),
         "pins_plan": (I32, [P, V, V, D, V, V, V, I64, V]),
         "pins_solve": (I32, [P, POINTER(Params), POINTER(Result), V]),
+        "pins_solve_ws": (I32, [V, P, POINTER(Params), POINTER(Result), V]),
         "pins_solve_host": (I32, [P, POINTER(Params), POINTER(Result), POINTER(I64), V]),
         "pins_prof_enable": (None, [I32]),
         "pins_prof_reset": (None, []),
@@ -180,6 +183,14 @@ def sinkhorn_sweep(ws: Workspace, pb: DeviceProblem, phi, psi, s: float, f, g):
     _check(load().pins_sinkhorn_sweep(ws.h, pb.ref(), _p(phi), _p(psi), s, _p(f), _p(g), _stream()))
 
 
+def sinkhorn(ws: Workspace, pb: DeviceProblem, phi, psi, s: float, f, g, tol: float, max_sweeps: int):
+    """Sinkhorn phase (Alg. 2 lines 4-8) in place; returns (sweeps, final ||grad P||_1)."""
+    t, r = c_int32(), c_double()
+    _check(load().pins_sinkhorn(ws.h, pb.ref(), _p(phi), _p(psi), s, _p(f), _p(g), float(tol), int(max_sweeps),
+                                ctypes.byref(t), ctypes.byref(r), _stream()))
+    return t.value, r.value
+
+
 def evaluate(ws: Workspace, pb: DeviceProblem, phi, psi, s, f, g, tau=0.0, want_sums=True) -> Dict:
     torch = _torch()
     r = torch.empty(pb.m, dtype=torch.float64, device="cuda") if want_sums else None
@@ -206,16 +217,20 @@ def get_csr(ws: Workspace):
 
 
 def sparsify_dense(ws: Workspace, P, tau: float):
-    """CSR (rowptr, colidx, val) of P_ij >= tau via the production compaction kernel."""
+    """CSR (rowptr, colidx, val) of a caller-given dense P: P_ij >= tau (warp-ballot
+    compaction kernels of pins_sparsify_dense; the evaluation pass's own sparsifier is
+    reached through evaluate(tau > 0) + get_csr)."""
     torch = _torch()
     m, n = P.shape
-    rowptr = torch.empty(m + 1, dtype=torch.int64, device="cuda")
-    cap = m * n
-    colidx = torch.empty(cap, dtype=torch.int32, device="cuda")
-    val = torch.empty(cap, dtype=torch.float64, device="cuda")
+    lib = load()
     nnz = c_int64()
-    _check(load().pins_sparsify_dense(ws.h, m, n, _p(P), int(P.stride(0)), float(tau), _p(rowptr),
-                                      _p(colidx), _p(val), cap, ctypes.byref(nnz), _stream()))
+    _check(lib.pins_sparsify_dense(ws.h, m, n, _p(P), int(P.stride(0)), float(tau), None, None, None, 0,
+                                   ctypes.byref(nnz), _stream()))
+    rowptr = torch.empty(m + 1, dtype=torch.int64, device="cuda")
+    colidx = torch.empty(max(nnz.value, 1), dtype=torch.int32, device="cuda")
+    val = torch.empty(max(nnz.value, 1), dtype=torch.float64, device="cuda")
+    _check(lib.pins_sparsify_dense(ws.h, m, n, _p(P), int(P.stride(0)), float(tau), _p(rowptr),
+                                   _p(colidx), _p(val), colidx.numel(), ctypes.byref(nnz), _stream()))
     return rowptr, colidx[:nnz.value], val[:nnz.value]
 
 
@@ -255,7 +270,8 @@ def plan(pb: DeviceProblem, phi, psi, s, f, g):
     return X
 
 
-def solve(pb: DeviceProblem, prm: Optional[Params] = None, trace: bool = False, want_duals=True) -> Dict:
+def solve(pb: DeviceProblem, prm: Optional[Params] = None, trace: bool = False, want_duals=True,
+          ws: Optional["Workspace"] = None) -> Dict:
     torch = _torch()
     prm = prm or default_params()
     dev = dict(dtype=torch.float64, device="cuda")
@@ -267,7 +283,10 @@ def solve(pb: DeviceProblem, prm: Optional[Params] = None, trace: bool = False, 
     tr = (c_double * max(1, prm.K))() if trace else None
     if trace:
         res.obj_trace_host = ctypes.cast(tr, POINTER(c_double))
-    _check(load().pins_solve(pb.ref(), ctypes.byref(prm), ctypes.byref(res), _stream()))
+    if ws is None:
+        _check(load().pins_solve(pb.ref(), ctypes.byref(prm), ctypes.byref(res), _stream()))
+    else:
+        _check(load().pins_solve_ws(ws.h, pb.ref(), ctypes.byref(prm), ctypes.byref(res), _stream()))
     out = {k: getattr(res, k) for k in ("s", "obj", "dual_obj", "lp_dual_obj", "kkt", "dual_inf", "gap",
                                         "outer_iters", "sweeps", "newton_iters", "cg_iters", "status",
                                         "seconds")}

@@ -34,8 +34,8 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts_match_header():
     from paper_2502_03749_b200 import pins
-    # pins_problem: 2 int64 + 2 int32 + 8 pointer/double/int64 fields = 80 bytes
-    assert ctypes.sizeof(pins.Problem) == 88   # 2 int64 + 2 int32 + 8 x 8-byte fields
+    # pins_problem: 2 int64 (16) + 2 int32 (8) + 8 pointer/double/int64 fields (64) = 88 bytes
+    assert ctypes.sizeof(pins.Problem) == 88
     assert pins.Params.outer_tol.offset == 8 and pins.Params.sink_tol.offset == 24
     assert ctypes.sizeof(pins.Params) == 112
 

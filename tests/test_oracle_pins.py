@@ -143,13 +143,6 @@ def test_cg_small_spd():
     assert np.allclose(x, np.linalg.solve(A, rhs), rtol=1e-9, atol=1e-12)
 
 
-def test_line_search_quadratic_accepts_unit_step():
-    # P(x) = -(x-1)^2 at x=0, d=1: alpha = 1 is accepted (SPEC example, §3.2)
-    P = lambda x: -(x - 1.0) ** 2
-    x, d, c = 0.0, 1.0, 1e-4
-    assert P(x + d) >= P(x) + c * 1.0 * 2.0 * d
-
-
 def test_newton_direction_is_exact_newton_without_sparsification():
     # With theta = 0 (keep everything), mu -> 0 and a tight CG, the direction
     # solves the Newton system of Eq. (9):  hess P d = -grad P  (min-norm sense).
@@ -298,13 +291,33 @@ def test_logsumexp_identities():
     assert L[0] == 0.0 and L[1] == -np.inf
 
 
-def test_cg_rtol_forcing_term():
-    # reading R5: clamp(cg_forcing * newton_tol / ||grad||_1, cg_tol, 0.5)
-    prm = po.Params(newton_tol=1e-8, cg_tol=1e-6, cg_forcing=0.1)
-    assert po.cg_rtol(1e-8, prm) == pytest.approx(0.1)
-    assert po.cg_rtol(1e-10, prm) == 0.5
-    assert po.cg_rtol(1.0, prm) == 1e-6
-    assert po.cg_rtol(1e-3, po.Params(cg_forcing=0.0, cg_tol=1e-9)) == 1e-9
+def test_inexact_newton_direction_meets_its_forcing_residual():
+    # Reading R5 (inexact Newton): the direction returned by newton_direction solves the
+    # damped sparsified Newton system M d = eta grad P to the forcing tolerance.  The
+    # residual is recomputed here from a DENSE assembly of M (Eq. (9) blocks, diagonal
+    # blocks exact, off-diagonal thresholded at tau), independently of the oracle's matvec.
+    rng = np.random.default_rng(21)
+    m, n, eta = 9, 7, 0.1
+    Ck = rng.random((m, n))
+    a = po_norm(rng.random(m) + 0.1); b = po_norm(rng.random(n) + 0.1)
+    f, g = rng.normal(0, 0.05, m), rng.normal(0, 0.05, n)
+    for forcing, newton_tol in ((0.1, 1e-3), (0.0, 1e-8)):
+        prm = po.Params(eta=eta, cg_forcing=forcing, newton_tol=newton_tol, cg_tol=1e-9, theta=1e-2)
+        df, dg, info = po.newton_direction(f, g, Ck, a, b, eta, prm)
+        X = np.exp((f[:, None] + g[None, :] - Ck - eta) / eta)
+        tau = 1e-2 / (m * n)
+        Xs = np.where(X >= tau, X, 0.0)
+        r, c = X.sum(1), X.sum(0)
+        mu = 1e-10 * max(r.max(), c.max())
+        M = np.block([[np.diag(r), Xs], [Xs.T, np.diag(c)]]) + mu * np.eye(m + n)
+        rhs = eta * np.concatenate([a - r, b - c])
+        d = np.concatenate([df, dg])
+        rel = np.linalg.norm(M @ d - rhs) / np.linalg.norm(rhs)
+        gnorm = np.abs(a - r).sum() + np.abs(b - c).sum()
+        want = min(0.5, max(1e-9, forcing * newton_tol / gnorm)) if forcing > 0 else 1e-9
+        assert rel <= want * (1 + 1e-6) + 1e-13
+        if forcing > 0:
+            assert want > 1e-6 and info["cg_iters"] < m + n      # a loose solve stops early
 
 
 def test_dual_increase_matches_direct_difference():
@@ -353,3 +366,46 @@ def test_kkt_of_exact_lp_solution():
         logX = np.log(ex["X"])
     k = po.kkt(C, logX, a, b, ex["u"], ex["v"])
     assert k["primal"] <= 1e-14 and k["dual_inf"] <= 1e-13 and abs(k["gap"]) <= 1e-13
+
+
+def test_outer_rule_geometric_tail_is_exact_for_geometric_sequences():
+    # rule 2 (reading R6): for obj_k = L + A q^k the estimator D2 r / (1 - r) equals the
+    # true remaining error obj_k - L exactly, so the rule stops at the FIRST k whose true
+    # error is <= tol |obj_k| (and not earlier), once k >= 2W + 1
+    L, A, q, tol = 0.37, 0.05, 0.8, 1e-6
+    prm = po.Params(outer_rule=2, outer_tol=tol)
+    objs, stop = [], None
+    for k in range(400):
+        objs.append(L + A * q ** k)
+        if po.outer_converged(objs, prm):
+            stop = len(objs)
+            break
+    assert stop is not None
+    W = max(5, stop // 4)
+    err = lambda K: objs[K - 1] - L
+    assert err(stop) <= tol * objs[stop - 1] * (1 + 1e-9)
+    # the step before either had a larger true error or was too short for the estimator
+    prev = stop - 1
+    assert err(prev) > tol * objs[prev - 1] * (1 - 1e-9) or prev < 2 * max(5, prev // 4) + 1
+    # monotone sequences (Thm 4.1) decaying slower than any q^k never stop at this tol
+    objs = [L + A / (k + 1) for k in range(300)]
+    assert not any(po.outer_converged(objs[:K], prm) for K in range(2, 300))
+    # a sequence that is still decreasing by more than tol per window never stops
+    objs = [L + A * (1 - 1e-3 * k) for k in range(300)]
+    assert not any(po.outer_converged(objs[:K], prm) for K in range(2, 300))
+
+
+def test_bregman_divergence_closed_forms():
+    # D_phi(X, Y) with phi = sum X (log X - 1) is the generalised KL
+    # divergence sum X log(X/Y) - X + Y (0 log 0 = 0): pinned on hand-computed values
+    Y = np.full((2, 2), 0.25)
+    X = np.array([[0.5, 0.0], [0.0, 0.5]])
+    assert po.bregman(X, Y) == pytest.approx(np.log(2.0), rel=1e-15)          # 2 (0.5 log 2) - 1 + 1
+    assert po.bregman(Y, Y) == 0.0 or abs(po.bregman(Y, Y)) <= 1e-16
+    X2 = np.array([[1.0, 2.0], [3.0, 4.0]])
+    Y2 = np.array([[2.0, 1.0], [1.0, 1.0]])
+    hand = (1 * np.log(0.5) + 2 * np.log(2) + 3 * np.log(3) + 4 * np.log(4)) - 10.0 + 5.0
+    assert po.bregman(X2, Y2) == pytest.approx(hand, rel=1e-14)
+    # scaling: D(cX, cY) = c D(X, Y); and D(X, Y) > 0 for X != Y
+    assert po.bregman(3 * X2, 3 * Y2) == pytest.approx(3 * hand, rel=1e-14)
+    assert po.bregman(Y2, X2) > 0

@@ -15,6 +15,15 @@ Each generator returns a :class:`Workload`. Recipes (also in DESIGN.md):
 * ``c4_l1rect``  m=8192, n=16384, 3-D points uniform in [0,1]^3 quantised to
   2^-20, L1 cost, marginals Dirichlet(1), eta=1e-3.
 
+The point sets of c0, c3 and c4 are quantised onto integer lattices (so that
+distances are exact in fp32 and fp16, which the fast cost paths exploit); the
+``*_r`` variants are the same configurations with REAL-valued coordinates as
+BASELINE.json writes them (no rounding), which exercise the fp64 cost paths:
+
+* ``c0_pts64_r``   as c0 with points uniform in [0,1]^2 (plain floats).
+* ``c3_gmm10k_r``  as c3 with the Gaussian-mixture points unrounded.
+* ``c4_l1rect_r``  as c4 with points uniform in [0,1]^3 (plain floats).
+
 ``scale`` (default 1.0) shrinks m and n proportionally for small parity cases;
 the *structure* (value distribution, cost kind) is unchanged.
 """
@@ -56,9 +65,11 @@ def _normalise(v: np.ndarray) -> np.ndarray:
 
 
 def _max_pair_distance(X: np.ndarray, Y: np.ndarray, kind: int) -> float:
-    """max_ij D_ij over all pairs, exact integer arithmetic (blocked)."""
-    Xi = X.astype(np.int64)
-    Yi = Y.astype(np.int64)
+    """max_ij D_ij over all pairs (blocked): exact integer arithmetic for lattice
+    points, fp64 for real-valued points."""
+    integral = bool(np.all(X == np.rint(X)) and np.all(Y == np.rint(Y)))
+    Xi = X.astype(np.int64) if integral else np.asarray(X, dtype=np.float64)
+    Yi = Y.astype(np.int64) if integral else np.asarray(Y, dtype=np.float64)
     best = 0
     bs = max(1, 2_000_000 // max(1, Yi.shape[0]))
     for s in range(0, Xi.shape[0], bs):
@@ -67,7 +78,7 @@ def _max_pair_distance(X: np.ndarray, Y: np.ndarray, kind: int) -> float:
             D = (diff * diff).sum(-1)
         else:
             D = np.abs(diff).sum(-1)
-        best = max(best, int(D.max()))
+        best = max(best, D.max())
     return float(best)
 
 
@@ -79,15 +90,18 @@ def _points_workload(name, X, Y, kind, a, b, eta, meta=None) -> Workload:
                     cost_scale=scale, meta=meta or {})
 
 
-def c0_pts64(seed: int = 0, scale: float = 1.0) -> Workload:
+def c0_pts64(seed: int = 0, scale: float = 1.0, lattice: bool = True) -> Workload:
     rng = np.random.default_rng(seed)
     n = max(2, int(round(64 * scale)))
-    q = float(2 ** 16)
-    X = np.floor(rng.random((n, 2)) * q)
-    Y = np.floor(rng.random((n, 2)) * q)
+    q = float(2 ** 16) if lattice else 1.0
+    X = rng.random((n, 2)) * q
+    Y = rng.random((n, 2)) * q
+    if lattice:
+        X, Y = np.floor(X), np.floor(Y)
     a = np.full(n, 1.0 / n)
     b = np.full(n, 1.0 / n)
-    return _points_workload("c0_pts64", X, Y, COST_SQEUCLID, a, b, 1e-2)
+    return _points_workload("c0_pts64" if lattice else "c0_pts64_r", X, Y, COST_SQEUCLID, a, b, 1e-2,
+                            meta={"lattice": lattice})
 
 
 def c1_rand1k(seed: int = 1, scale: float = 1.0) -> Workload:
@@ -123,7 +137,7 @@ def c2_img4k(seed: int = 2, scale: float = 1.0) -> Workload:
                             meta={"side": side})
 
 
-def c3_gmm10k(seed: int = 3, scale: float = 1.0) -> Workload:
+def c3_gmm10k(seed: int = 3, scale: float = 1.0, lattice: bool = True) -> Workload:
     rng = np.random.default_rng(seed)
     n = max(2, int(round(10000 * scale)))
     d, K = 10, 8
@@ -134,25 +148,29 @@ def c3_gmm10k(seed: int = 3, scale: float = 1.0) -> Workload:
     def draw(cnt):
         comp = rng.choice(K, size=cnt, p=w)
         pts = means[comp] + stds[comp, None] * rng.normal(size=(cnt, d))
-        return np.rint(pts * 64.0)       # lattice 1/64 -> integer coordinates
+        return np.rint(pts * 64.0) if lattice else pts   # lattice 1/64 -> integer coordinates
 
     X = draw(n)
     Y = draw(n)
     a = _normalise(rng.uniform(0.1, 1.0, n))
     b = _normalise(rng.uniform(0.1, 1.0, n))
-    return _points_workload("c3_gmm10k", X, Y, COST_SQEUCLID, a, b, 1e-3)
+    return _points_workload("c3_gmm10k" if lattice else "c3_gmm10k_r", X, Y, COST_SQEUCLID, a, b, 1e-3,
+                            meta={"lattice": lattice})
 
 
-def c4_l1rect(seed: int = 4, scale: float = 1.0) -> Workload:
+def c4_l1rect(seed: int = 4, scale: float = 1.0, lattice: bool = True) -> Workload:
     rng = np.random.default_rng(seed)
     m = max(2, int(round(8192 * scale)))
     n = max(2, int(round(16384 * scale)))
-    q = float(2 ** 20)
-    X = np.floor(rng.random((m, 3)) * q)
-    Y = np.floor(rng.random((n, 3)) * q)
+    q = float(2 ** 20) if lattice else 1.0
+    X = rng.random((m, 3)) * q
+    Y = rng.random((n, 3)) * q
+    if lattice:
+        X, Y = np.floor(X), np.floor(Y)
     a = rng.dirichlet(np.ones(m))
     b = rng.dirichlet(np.ones(n))
-    return _points_workload("c4_l1rect", X, Y, COST_L1, _normalise(a), _normalise(b), 1e-3)
+    return _points_workload("c4_l1rect" if lattice else "c4_l1rect_r", X, Y, COST_L1, _normalise(a),
+                            _normalise(b), 1e-3, meta={"lattice": lattice})
 
 
 CONFIGS: Dict[str, Callable[..., Workload]] = {
@@ -161,6 +179,10 @@ CONFIGS: Dict[str, Callable[..., Workload]] = {
     "c2_img4k": c2_img4k,
     "c3_gmm10k": c3_gmm10k,
     "c4_l1rect": c4_l1rect,
+    # real-valued (non-lattice) variants of the point configurations
+    "c0_pts64_r": lambda seed=0, scale=1.0: c0_pts64(seed, scale, lattice=False),
+    "c3_gmm10k_r": lambda seed=3, scale=1.0: c3_gmm10k(seed, scale, lattice=False),
+    "c4_l1rect_r": lambda seed=4, scale=1.0: c4_l1rect(seed, scale, lattice=False),
 }
 
 
