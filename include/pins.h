@@ -66,7 +66,8 @@ typedef struct pins_problem {
  * Defaults (pins_default_params) follow PAPER.md Appendix A.2 (lines 477-485). */
 typedef struct pins_params {
     int32_t K;               /* max EPPA (outer) iterations               (500)   */
-    int32_t outer_rule;      /* 0 rel. change, 1 halving, 2 geometric tail (0)   */
+    int32_t outer_rule;      /* 0 rel. change, 1 halving, 2 geometric tail,
+                                3 certified: LP gap <= outer_tol |obj| (0)   */
     double outer_tol;        /* outer tolerance                           (1e-4)  */
     int32_t T1;              /* max Sinkhorn sweeps per subproblem        (50000) */
     double sink_tol;         /* Sinkhorn phase: ||grad P||_1 threshold    (6.3e-4)*/
@@ -186,24 +187,48 @@ int pins_residuals(pins_workspace *ws, const pins_problem *pb, const double *phi
                    const double *psi, double s, const double *f, const double *g,
                    double *u, double *v, double *res_host, void *stream);
 
+/* LP certificate of the plan X~(f,g) at centre (phi, psi, s) (reading R11,
+ * DESIGN.md §3; LP duality of Eq. (1)): evaluation with the
+ * plan block sparsified at tau = prm->theta/(m n); maximum-weight spanning
+ * forest of that support (the LP optimum is a vertex, whose
+ * support is a forest); tree duals u_i + v_j = C_ij on the forest; row then
+ * column c-transforms u_i = min_j C_ij - v_j, v_j = min_i C_ij - u_i (dual
+ * feasible by construction); the entropic duals are the fallback candidate.
+ * u (m), v (n): device outputs, may be NULL.  cert_host (>= 8 doubles):
+ * [0] ||Xe-a||_1 + ||X^Te-b||_1, [1] <C,X>, [2] <a,u> + <b,v> (<= LP*),
+ * [3] gap = [1] - [2], [4] measured max(0, max_ij u_i + v_j - C_ij),
+ * [5] forest edges (0: no forest built, m + n > 26000), [6] 1 if the forest's
+ * duals gave the bound, [7] nnz of the sparsified support.  Synchronises.  */
+int pins_lp_certificate(pins_workspace *ws, const pins_problem *pb, const pins_params *prm,
+                        const double *phi, const double *psi, double s, const double *f, const double *g,
+                        double *u, double *v, double *cert_host, void *stream);
+
 /* Materialise X~(f,g) densely (device m x n, leading dim ldx).  Asynchronous. */
 int pins_plan(const pins_problem *pb, const double *phi, const double *psi, double s,
               const double *f, const double *g, double *X, int64_t ldx, void *stream);
 
 /* Output of pins_solve.  Device arrays are caller-owned (f, g, phi, psi: sizes
- * m, n, m, n; u, v optional).  Scalars are written on the host.              */
+ * m, n, m, n; u, v optional).  Scalars are written on the host.
+ * LP KKT of the returned plan X = X~(f, g) (reading R11):
+ * kkt = primal residual, dual_inf = measured dual infeasibility of (u, v),
+ * gap = <C, X> - lp_dual_obj; (u, v) are CERTIFIED duals -- dual feasible by
+ * construction (c-transforms of the tree duals of the plan's maximum-weight
+ * spanning forest, or of the entropic duals, whichever bound is larger), so
+ * lp_dual_obj <= LP* (weak duality) and gap bounds the objective error.     */
 typedef struct pins_result {
     double *f, *g;           /* last subproblem potentials (device)              */
     double *phi, *psi;       /* proximal centre log form (device)                */
-    double *u, *v;           /* LP dual estimates (device, may be NULL)          */
+    double *u, *v;           /* certified LP duals (device, may be NULL)         */
     double s;                /* centre scale s_K                                 */
     double obj;              /* <C, X>  (primal objective of the returned plan)  */
     double dual_obj;         /* P^k(f,g) of the last subproblem (Eq. (8))        */
-    double lp_dual_obj;      /* <a,u> + <b,v>                                    */
-    double kkt;              /* ||Xe-a||_1 + ||X^Te-b||_1  (reading R8)          */
-    double dual_inf;         /* max(0, max_ij u_i + v_j - C_ij)                  */
+    double lp_dual_obj;      /* <a,u> + <b,v>  (a certified lower bound on LP*)  */
+    double kkt;              /* ||Xe-a||_1 + ||X^Te-b||_1  (primal residual)     */
+    double dual_inf;         /* max(0, max_ij u_i + v_j - C_ij)  (measured)      */
     double gap;              /* obj - lp_dual_obj                                */
     int32_t outer_iters, sweeps, newton_iters, cg_iters, status; /* status 0 = converged, 1 = budget */
+    int32_t certificates;    /* LP certificates built during the solve           */
+    int32_t cert_tree;       /* 1: the returned duals are the tree-basis ones    */
     double *obj_trace_host;  /* optional host array of length >= K (may be NULL) */
     double seconds;          /* host wall time of the solve                      */
 } pins_result;

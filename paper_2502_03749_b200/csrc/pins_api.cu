@@ -17,6 +17,7 @@
 #include "pins_order.cuh"
 #include "pins_tree.cuh"
 #include "pins_treecl.cuh"
+#include "pins_cert.cuh"
 
 using namespace pins;
 
@@ -179,6 +180,9 @@ struct pins_workspace {
     int tree_last_its = 0, tree_backoff = 0;
     const int *tree_rstart = nullptr, *tree_ctr = nullptr;
     const double *tree_frec = nullptr;
+    TreeArgs tree_last;                // arguments of the last tree build (certificate replay)
+    // LP certificate (pins_cert.cuh): tree-dual scratch, c-transform partials, candidates
+    DevBuf cz, cdd, cdf, ctc, cpart, cu0, cv0, cu1, cv1, cbu, cbv, crow;
     bool csr_ready = false, csc_ready = false;
     bool x0_enable = false;    // solve_core: warm-start the cluster tree-PCG from the previous direction
     bool dir_valid = false;    // ws->dir holds the previous Newton system's solution
@@ -888,7 +892,7 @@ bool use_tree_cg(pins_workspace *ws, long long m, long long n) {
 
 int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const double *rhs, double *x,
                 double rtol, int maxit, const double *gradf, const double *gradg, const double *a,
-                const double *b, cudaStream_t st, int setup_only = 0) {
+                const double *b, cudaStream_t st, int setup_only = 0, bool force_rebuild = false) {
     const long long N = m + n, nnz = std::max<long long>(ws->nnz, 1);
     PINS_TRY(ensure(ws->cgst, sizeof(double) * 16));
     // persistent arrays first, nnz-sized scratch last (offsets stay put as nnz changes)
@@ -963,11 +967,12 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     A.best = ptr<unsigned long long>(ws->tr_u64);
     // reuse the stored tree while it keeps CG short (the kernel also checks that
     // every tree edge is still in the support and rebuilds otherwise)
-    A.reuse = ws->tree_valid && ws->tree_last_its <= 48 ? 1 : 0;
+    A.reuse = ws->tree_valid && ws->tree_last_its <= 48 && !force_rebuild ? 1 : 0;
     A.setup_only = setup_only;
     ws->tree_rstart = A.rstart;
     ws->tree_ctr = A.ctr;
     ws->tree_frec = A.frec;
+    ws->tree_last = A;
     const size_t base = sizeof(double) * (size_t)N;
     const size_t budget = 220 * 1024;
     A.tail_cap = base < budget ? (int)((budget - base) / 40) : 0;
@@ -1032,6 +1037,133 @@ int run_cg_tree_cluster(pins_workspace *ws, long long m, long long n, double mu,
     }
     LAUNCH(PINS_PROF_CG, st, cg_tree_cluster_kernel<<<kCGC, kCGT, smem, st>>>(A));
     PINS_CUDA(cudaGetLastError());
+    return PINS_OK;
+}
+
+// ------------------------------------------------------------ LP certificate
+// (reading R11; pins_cert.cuh).  c-transform of `pin` over the cost: orient 0
+// (rows of C): out_i = min_j (C_ij - pin_j); orient 1 (columns): out_j =
+// min_i (C_ij - pin_i).  mode 1: out_p = max_q (self_p + pin_q - C_pq).
+int ctrans(pins_workspace *ws, const pins_problem *pb, int orient, int mode, const double *pin,
+           const double *self, double *out, cudaStream_t st) {
+    const bool dense = pb->cost_kind == PINS_COST_DENSE;
+    CtArgs A;
+    memset(&A, 0, sizeof A);
+    A.M = orient == 0 ? pb->m : pb->n;
+    A.N = orient == 0 ? pb->n : pb->m;
+    A.orient = orient;
+    A.mode = mode;
+    A.cd = make_cd(pb);
+    if (!dense && orient == 1) std::swap(A.cd.x, A.cd.y);
+    A.scale = pb->cost_scale;
+    A.pin = pin;
+    A.self = self;
+    const long long RB = dense && orient == 0 ? (A.M + 3) / 4 : (A.M + kCtT - 1) / kCtT;
+    long long S = (4LL * ws->nsm + RB - 1) / RB;
+    S = std::max(1LL, std::min(S, std::max(1LL, A.N / 64)));
+    A.S = (int)S;
+    PINS_TRY(ensure(ws->cpart, sizeof(double) * S * A.M));
+    A.part = ptr<double>(ws->cpart);
+    const int grid = (int)(RB * S);
+    if (dense && orient == 0) LAUNCH(PINS_PROF_VEC, st, ctrans_dense_rows_kernel<<<grid, kCtT, 0, st>>>(A));
+    else if (dense) LAUNCH(PINS_PROF_VEC, st, ctrans_dense_cols_kernel<<<grid, kCtT, 0, st>>>(A));
+    else if (pb->cost_kind == PINS_COST_SQEUCLID) LAUNCH(PINS_PROF_VEC, st, ctrans_points_kernel<1><<<grid, kCtT, 0, st>>>(A));
+    else LAUNCH(PINS_PROF_VEC, st, ctrans_points_kernel<2><<<grid, kCtT, 0, st>>>(A));
+    LAUNCH(PINS_PROF_VEC, st, ctrans_finalize_kernel<<<grid_1d(A.M, ws->nsm), 256, 0, st>>>(A.M, A.S, mode,
+                                                                                        A.part, out));
+    PINS_CUDA(cudaGetLastError());
+    return PINS_OK;
+}
+
+struct CertOut {
+    double primal = 0, pobj = 0, dobj = -INFINITY, gap = INFINITY, dual_inf = -1;
+    int tree_edges = 0, used_tree = 0;
+    long long nnz = 0;
+};
+
+// <a,u> + <b,v> on the device (deterministic), read back (synchronises)
+int dual_value(pins_workspace *ws, const pins_problem *pb, const double *u, const double *v, double *out,
+               cudaStream_t st) {
+    LAUNCH(PINS_PROF_REDUCE, st, dots_kernel<<<1, 1024, 0, st>>>(pb->m, pb->n, pb->a, u, pb->b, v,
+                                                                 ptr<double>(ws->rowsum), ptr<double>(ws->colsum),
+                                                                 ptr<double>(ws->st)));
+    PINS_CUDA(cudaMemcpyAsync(ws->h + 24, ptr<double>(ws->st) + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
+    PINS_CUDA(cudaStreamSynchronize(st));
+    *out = ws->h[24];
+    return PINS_OK;
+}
+
+// Measured dual infeasibility of the certified duals: max(0, max_ij u_i + v_j - C_ij)
+// (one more pass; the c-transforms make it 0 up to rounding).  Synchronises.
+int measure_dual_inf(pins_workspace *ws, const pins_problem *pb, CertOut *co, cudaStream_t st) {
+    PINS_TRY(ctrans(ws, pb, 0, 1, ptr<double>(ws->cbv), ptr<double>(ws->cbu), ptr<double>(ws->crow), st));
+    LAUNCH(PINS_PROF_REDUCE, st, vec_max_kernel<<<1, 1024, 0, st>>>(pb->m, ptr<double>(ws->crow), ptr<double>(ws->st), 12));
+    PINS_CUDA(cudaMemcpyAsync(ws->h + 25, ptr<double>(ws->st) + 12, sizeof(double), cudaMemcpyDeviceToHost, st));
+    PINS_CUDA(cudaStreamSynchronize(st));
+    co->dual_inf = ws->h[25];
+    return PINS_OK;
+}
+
+// Certificate of the plan X~(f, g) at centre (phi, psi, s), whose evaluation
+// (sums, CSR / CSC at tau) is the workspace state `cur` (reading R11): basis
+// forest -> tree duals -> row / column c-transforms; the entropic duals
+// ((f + phi)/s, (g + psi - eta)/s) are the second candidate; the larger
+// certified bound wins.  Certified duals -> ws->cbu / cbv.
+int certify(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi, double s,
+            const double *f, const double *g, const EvalOut &cur, bool want_dual_inf, CertOut *co,
+            cudaStream_t st, double target_gap = -INFINITY) {
+    *co = CertOut();
+    const long long m = pb->m, n = pb->n, N = m + n;
+    PINS_TRY(prepare(ws, pb));
+    for (DevBuf *b : {&ws->cu0, &ws->cu1, &ws->cbu, &ws->crow}) PINS_TRY(ensure(*b, sizeof(double) * std::max(m, n)));
+    for (DevBuf *b : {&ws->cv0, &ws->cv1, &ws->cbv}) PINS_TRY(ensure(*b, sizeof(double) * n));
+    co->primal = cur.gnorm;
+    co->pobj = cur.cost;
+    co->nnz = ws->nnz;
+    double *u0 = ptr<double>(ws->cu0), *v0 = ptr<double>(ws->cv0);
+    double *u1 = ptr<double>(ws->cu1), *v1 = ptr<double>(ws->cv1);
+    for (int cand = 0; cand < 2; ++cand) {
+        if (cand == 0) {                            // tree duals of the basis forest
+            if (!(N <= kTreeMaxNodes && ws->csr_ready && ws->csc_ready && ws->nnz >= 1)) continue;
+            PINS_TRY(run_cg_tree(ws, m, n, 0.0, ptr<double>(ws->rhs), ptr<double>(ws->uv), 0.5, 1, nullptr,
+                                 nullptr, nullptr, nullptr, st, 1, true));
+            for (DevBuf *b : {&ws->cz, &ws->cdd, &ws->cdf, &ws->ctc}) PINS_TRY(ensure(*b, sizeof(double) * N));
+            const TreeArgs &T = ws->tree_last;
+            TreeDualArgs D;
+            D.m = (int)m; D.n = (int)n;
+            D.ctr = T.ctr; D.rstart = T.rstart;
+            D.fu = T.fu; D.fv1 = T.fv1; D.fv2 = T.fv2; D.fs1 = T.fs1; D.fs2 = T.fs2;
+            D.tei = T.tei; D.tej = T.tej;
+            D.cd = make_cd(pb);
+            D.scale = pb->cost_scale;
+            D.dd = ptr<double>(ws->cdd); D.df = ptr<double>(ws->cdf); D.tc = ptr<double>(ws->ctc);
+            D.z = ptr<double>(ws->cz);
+            LAUNCH(PINS_PROF_VEC, st, tree_duals_kernel<<<1, 1024, 0, st>>>(D));
+            LAUNCH(PINS_PROF_VEC, st, split_duals_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(m, n, D.z, u0, v0));
+            PINS_CUDA(cudaGetLastError());
+            int te = 0;
+            PINS_CUDA(cudaMemcpyAsync(&te, T.ctr + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+            PINS_CUDA(cudaStreamSynchronize(st));
+            co->tree_edges = te;
+        } else {                                    // entropic duals (reading R8)
+            LAUNCH(PINS_PROF_VEC, st, lp_duals_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(
+                m, n, pb->eta, 1.0 / s, f, g, phi, psi, u0, v0));
+            PINS_CUDA(cudaGetLastError());
+        }
+        PINS_TRY(ctrans(ws, pb, 0, 0, v0, nullptr, u1, st));      // u'_i = min_j C_ij - v_j
+        PINS_TRY(ctrans(ws, pb, 1, 0, u1, nullptr, v1, st));      // v'_j = min_i C_ij - u'_i
+        double D = 0.0;
+        PINS_TRY(dual_value(ws, pb, u1, v1, &D, st));
+        if (std::isfinite(D) && D > co->dobj) {
+            co->dobj = D;
+            co->used_tree = cand == 0 ? 1 : 0;
+            PINS_CUDA(cudaMemcpyAsync(ws->cbu.p, u1, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+            PINS_CUDA(cudaMemcpyAsync(ws->cbv.p, v1, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        }
+        if (co->pobj - co->dobj <= target_gap) break;   // the basis duals already certify the target
+    }
+    co->gap = co->pobj - co->dobj;
+    if (want_dual_inf) PINS_TRY(measure_dual_inf(ws, pb, co, st));
     return PINS_OK;
 }
 
@@ -1360,6 +1492,33 @@ extern "C" int pins_residuals(pins_workspace *ws, const pins_problem *pb, const 
     return PINS_OK;
 }
 
+extern "C" int pins_lp_certificate(pins_workspace *ws, const pins_problem *pb, const pins_params *prm,
+                                   const double *phi, const double *psi, double s, const double *f, const double *g,
+                                   double *u, double *v, double *cert_host, void *stream) {
+    PINS_ARG(ws && prm && cert_host, "ws, prm, cert");
+    PINS_TRY(check_problem(pb));
+    invalidate_problem(ws);
+    PINS_ARG(phi && psi && f && g && s > 0.0, "phi, psi, f, g, s > 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    const double tau = prm->theta / ((double)pb->m * (double)pb->n);
+    EvalOut e;
+    PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &e));
+    CertOut co;
+    PINS_TRY(certify(ws, pb, phi, psi, s, f, g, e, true, &co, st));
+    if (u) PINS_CUDA(cudaMemcpyAsync(u, ws->cbu.p, sizeof(double) * pb->m, cudaMemcpyDeviceToDevice, st));
+    if (v) PINS_CUDA(cudaMemcpyAsync(v, ws->cbv.p, sizeof(double) * pb->n, cudaMemcpyDeviceToDevice, st));
+    PINS_CUDA(cudaStreamSynchronize(st));
+    cert_host[0] = co.primal;
+    cert_host[1] = co.pobj;
+    cert_host[2] = co.dobj;
+    cert_host[3] = co.gap;
+    cert_host[4] = co.dual_inf;
+    cert_host[5] = (double)co.tree_edges;
+    cert_host[6] = (double)co.used_tree;
+    cert_host[7] = (double)co.nnz;
+    return PINS_OK;
+}
+
 extern "C" int pins_plan(const pins_problem *pb, const double *phi, const double *psi, double s,
                          const double *f, const double *g, double *X, int64_t ldx, void *stream) {
     PINS_TRY(check_problem(pb));
@@ -1411,7 +1570,9 @@ static int solve_core(pins_workspace *ws, const pins_problem *pb, const pins_par
     int sweeps = 0, newton_its = 0, cg_its = 0, k = 0;
     bool converged = false;
     EvalOut cur;
-    double s_last = s;
+    CertOut cert;
+    int cert_k = -1, next_cert = 8, n_certs = 0;
+    bool halving_seen = false;
     FILE *trace = nullptr;
     if (const char *tp = getenv("PINS_TRACE")) trace = fopen(tp, "w");
     auto tk0 = std::chrono::steady_clock::now();
@@ -1471,11 +1632,38 @@ static int solve_core(pins_workspace *ws, const pins_problem *pb, const pins_par
         res->obj = cur.cost;
         res->kkt = cur.gnorm;
         res->dual_obj = cur.dualP;
-        res->dual_inf = std::max(0.0, pb->eta / s * cur.maxz);
-        s_last = s;
+        // outer stop (reading R6); rule 3 = certified (reading R11): the LP certificate of
+        // X^{k+1} = X~(f, g) is built when the halving estimator first fires and on a
+        // geometric schedule, and the solve stops once the primal residual is <= newton_tol
+        // and the certified gap <= outer_tol |<C, X>|
+        bool stop = false;
+        const bool last = k + 1 >= prm->K;
+        if (prm->outer_rule == 3) {
+            pins_params p1 = *prm;
+            p1.outer_rule = 1;
+            const bool halving = outer_converged(objs, &p1);
+            const bool trigger = k + 1 >= next_cert || (halving && !halving_seen);
+            halving_seen = halving_seen || halving;
+            if (trigger && cur.gnorm <= prm->newton_tol) {
+                const double target = prm->outer_tol * std::fabs(cur.cost);
+                PINS_TRY(certify(ws, pb, phi, psi, s, f, g, cur, false, &cert, st, target));
+                cert_k = k;
+                ++n_certs;
+                if (cert.gap <= target) stop = true;
+                else next_cert = k + 1 + std::max(8, (k + 1) / 8);
+            }
+        } else {
+            stop = outer_converged(objs, prm);
+        }
+        if ((stop || last) && cert_k != k) {        // the returned plan's certificate (report)
+            PINS_TRY(certify(ws, pb, phi, psi, s, f, g, cur, false, &cert, st));
+            cert_k = k;
+            ++n_certs;
+        }
+        if (stop || last) PINS_TRY(measure_dual_inf(ws, pb, &cert, st));
         // X^{k+1} = X~(f, g): centre update (Alg. 2 line 16), then C^{k+1} (line 3)
         PINS_TRY(pins_center_update(pb, phi, psi, &s, f, g, stream));
-        if (outer_converged(objs, prm)) {
+        if (stop) {
             converged = true;
             ++k;
             break;
@@ -1483,25 +1671,15 @@ static int solve_core(pins_workspace *ws, const pins_problem *pb, const pins_par
     }
     if (trace) fclose(trace);
     if (k > prm->K) k = prm->K;
-    // LP dual estimates of X^{K} (reading R8): u = phi/s_last, v = psi/s_last
-    // (phi, psi are already the updated centre; f, g folded in).
-    {
-        const double inv = 1.0 / s_last;
-        double *uu = res->u ? res->u : nullptr;
-        double *vv = res->v ? res->v : nullptr;
-        PINS_TRY(prepare(ws, pb));
-        if (!uu) uu = ptr<double>(ws->uv);
-        if (!vv) vv = ptr<double>(ws->uv) + m;
-        LAUNCH(PINS_PROF_VEC, st, scale_concat_kernel<<<grid_1d(m + n, ws->nsm), 256, 0, st>>>(m, n, inv, phi, psi, ptr<double>(ws->dir)));
-        PINS_CUDA(cudaMemcpyAsync(uu, ptr<double>(ws->dir), sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
-        PINS_CUDA(cudaMemcpyAsync(vv, ptr<double>(ws->dir) + m, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-        LAUNCH(PINS_PROF_REDUCE, st, dots_kernel<<<1, 1024, 0, st>>>(m, n, pb->a, uu, pb->b, vv, ptr<double>(ws->rowsum),
-                                        ptr<double>(ws->colsum), ptr<double>(ws->st)));
-        PINS_CUDA(cudaMemcpyAsync(ws->h, ws->st.p, 11 * sizeof(double), cudaMemcpyDeviceToHost, st));
-        PINS_CUDA(cudaStreamSynchronize(st));
-        res->lp_dual_obj = ws->h[8];
-        res->gap = res->obj - res->lp_dual_obj;
-    }
+    // certified LP duals of the returned plan X^K (reading R11): dual feasible by
+    // construction; lp_dual_obj <= LP* and gap = <C, X^K> - lp_dual_obj
+    if (res->u) PINS_CUDA(cudaMemcpyAsync(res->u, ws->cbu.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+    if (res->v) PINS_CUDA(cudaMemcpyAsync(res->v, ws->cbv.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    res->lp_dual_obj = cert.dobj;
+    res->gap = cert.gap;
+    res->dual_inf = cert.dual_inf;
+    res->certificates = n_certs;
+    res->cert_tree = cert.used_tree;
     res->s = s;
     res->outer_iters = k;
     res->sweeps = sweeps;
@@ -1605,6 +1783,7 @@ static int solve_entry(pins_workspace *ws, const pins_problem *pb, const pins_pa
     PINS_TRY(check_problem(pb));
     PINS_ARG(prm && res && res->f && res->g && res->phi && res->psi, "params / result buffers");
     PINS_ARG(prm->K >= 1 && prm->T2 >= 0 && prm->T1 >= 0, "budgets");
+    PINS_ARG(prm->outer_rule >= 0 && prm->outer_rule <= 3, "outer_rule in 0..3");
     auto t0 = std::chrono::steady_clock::now();
     cudaStream_t st = (cudaStream_t)stream;
     const long long m = pb->m, n = pb->n;

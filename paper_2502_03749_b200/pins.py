@@ -21,7 +21,7 @@ COST_DENSE, COST_SQEUCLID, COST_L1 = 0, 1, 2
 EXPORTS = [
     "pins_default_params", "pins_workspace_create", "pins_workspace_destroy", "pins_last_error",
     "pins_center_init", "pins_center_update", "pins_sinkhorn_sweep", "pins_sinkhorn", "pins_evaluate",
-    "pins_get_csr", "pins_sparsify_dense", "pins_cg", "pins_newton_step", "pins_residuals", "pins_plan", "pins_solve",
+    "pins_get_csr", "pins_sparsify_dense", "pins_cg", "pins_newton_step", "pins_residuals", "pins_lp_certificate", "pins_plan", "pins_solve",
     "pins_prof_enable", "pins_prof_reset", "pins_prof_read", "pins_prof_read_work", "pins_solve_host",
     "pins_solve_ws",
 ]
@@ -47,7 +47,8 @@ class Result(ctypes.Structure):
                 ("dual_obj", c_double), ("lp_dual_obj", c_double), ("kkt", c_double),
                 ("dual_inf", c_double), ("gap", c_double), ("outer_iters", c_int32),
                 ("sweeps", c_int32), ("newton_iters", c_int32), ("cg_iters", c_int32),
-                ("status", c_int32), ("obj_trace_host", POINTER(c_double)), ("seconds", c_double)]
+                ("status", c_int32), ("certificates", c_int32), ("cert_tree", c_int32),
+                ("obj_trace_host", POINTER(c_double)), ("seconds", c_double)]
 
 
 _lib = None
@@ -80,6 +81,7 @@ def load():
         "pins_newton_step": (I32, [V, P, POINTER(Params), V, V, D, V, V, POINTER(D), V]),
         "pins_residuals": (I32, [V, P, V, V, D, V, V, V, V, POINTER(D), V]),
         "pins_plan": (I32, [P, V, V, D, V, V, V, I64, V]),
+        "pins_lp_certificate": (I32, [V, P, POINTER(Params), V, V, D, V, V, V, V, POINTER(D), V]),
         "pins_solve": (I32, [P, POINTER(Params), POINTER(Result), V]),
         "pins_solve_ws": (I32, [V, P, POINTER(Params), POINTER(Result), V]),
         "pins_solve_host": (I32, [P, POINTER(Params), POINTER(Result), POINTER(I64), V]),
@@ -263,6 +265,18 @@ def residuals(ws: Workspace, pb: DeviceProblem, phi, psi, s, f, g) -> Dict:
     return dict(kkt=out[0], dual_inf=out[1], obj=out[2], lp_dual_obj=out[3], gap=out[4], u=u, v=v)
 
 
+def lp_certificate(ws: Workspace, pb: DeviceProblem, prm: Params, phi, psi, s, f, g) -> Dict:
+    """LP certificate of X~(f, g) (reading R11): certified duals u, v and the LP KKT."""
+    torch = _torch()
+    u = torch.empty(pb.m, dtype=torch.float64, device="cuda")
+    v = torch.empty(pb.n, dtype=torch.float64, device="cuda")
+    out = (c_double * 8)()
+    _check(load().pins_lp_certificate(ws.h, pb.ref(), ctypes.byref(prm), _p(phi), _p(psi), s, _p(f), _p(g),
+                                      _p(u), _p(v), out, _stream()))
+    return dict(primal=out[0], pobj=out[1], dual_obj=out[2], gap=out[3], dual_inf=out[4],
+                tree_edges=int(out[5]), used_tree=int(out[6]), nnz=int(out[7]), u=u, v=v)
+
+
 def plan(pb: DeviceProblem, phi, psi, s, f, g):
     torch = _torch()
     X = torch.empty(pb.m, pb.n, dtype=torch.float64, device="cuda")
@@ -289,7 +303,7 @@ def solve(pb: DeviceProblem, prm: Optional[Params] = None, trace: bool = False, 
         _check(load().pins_solve_ws(ws.h, pb.ref(), ctypes.byref(prm), ctypes.byref(res), _stream()))
     out = {k: getattr(res, k) for k in ("s", "obj", "dual_obj", "lp_dual_obj", "kkt", "dual_inf", "gap",
                                         "outer_iters", "sweeps", "newton_iters", "cg_iters", "status",
-                                        "seconds")}
+                                        "certificates", "cert_tree", "seconds")}
     out.update(f=f, g=g, phi=phi, psi=psi, u=u, v=v)
     if trace:
         out["trace"] = [tr[i] for i in range(res.outer_iters)]
@@ -345,6 +359,6 @@ def solve_host(hp: HostProblem, prm: Optional[Params] = None) -> Dict:
     _check(load().pins_solve_host(ctypes.byref(hp.struct), ctypes.byref(prm), ctypes.byref(res), io, _stream()))
     out = {k: getattr(res, k) for k in ("s", "obj", "dual_obj", "lp_dual_obj", "kkt", "dual_inf", "gap",
                                         "outer_iters", "sweeps", "newton_iters", "cg_iters", "status",
-                                        "seconds")}
+                                        "certificates", "cert_tree", "seconds")}
     out.update(h2d_bytes=io[0], d2h_bytes=io[1])
     return out
