@@ -288,9 +288,12 @@ int pins_solve_host(const pins_problem *pb_host, const pins_params *prm, pins_re
 void pins_prof_enable(int32_t on);
 void pins_prof_reset(void);
 int pins_prof_read(int32_t cls, int64_t *launches, double *ms);
-/* Algorithmic work the host attributed to a class since the last reset: for
- * PINS_PROF_CG the bytes of every iteration's sparse products and vector
- * streams (24 B x nnz + 80 B x (m + n) per iteration); 0 for other classes.  */
+/* Work attributed to a class since the last reset: for PINS_PROF_CG the bytes
+ * of every iteration's sparse products and vector streams (24 B x nnz + 80 B x
+ * (m + n) per iteration, counted by the host); for PINS_PROF_SWEEP_ROW (all
+ * half-sweeps) and PINS_PROF_EVAL (sum passes) the number of plan entries that
+ * survived the skip test and were evaluated exactly (counted on the device
+ * while profiling is enabled; synchronises); 0 for other classes.           */
 int pins_prof_read_work(int32_t cls, double *work);
 
 #ifdef __cplusplus

@@ -104,11 +104,18 @@ struct ProfScope {
 extern "C" void pins_prof_enable(int32_t on) { g_prof.on = on != 0; }
 extern "C" void pins_prof_reset(void) {
     g_prof.fold();
+    const unsigned long long z[2] = {0, 0};
+    cudaMemcpyToSymbol(pins::g_surv, z, sizeof z);
     for (int c = 0; c < PINS_PROF_NCLASS; ++c) { g_prof.launches[c] = 0; g_prof.ms[c] = 0.0; g_prof.work[c] = 0.0; }
 }
 extern "C" int pins_prof_read_work(int32_t cls, double *work) {
     PINS_ARG(cls >= 0 && cls < PINS_PROF_NCLASS && work, "class / pointer");
     *work = g_prof.work[cls];
+    if (cls == PINS_PROF_SWEEP_ROW || cls == PINS_PROF_EVAL) {     // survivors counted on the device
+        unsigned long long sv[2] = {0, 0};
+        PINS_CUDA(cudaMemcpyFromSymbol(sv, pins::g_surv, sizeof sv));
+        *work = (double)sv[cls == PINS_PROF_SWEEP_ROW ? 0 : 1];
+    }
     return PINS_OK;
 }
 extern "C" int pins_prof_read(int32_t cls, int64_t *launches, double *ms) {
@@ -571,6 +578,7 @@ void base_args(pins_workspace *ws, const pins_problem *pb, double s, PassArgs &A
     A.gticket = ptr<unsigned>(ws->gticket);
     A.st = ptr<double>(ws->pst);
     A.ctl = ptr<int>(ws->ctl);
+    A.count_surv = g_prof.on ? 1 : 0;
 }
 
 // One Sinkhorn half-sweep: o = 0 updates f (Alg. 2 line 5), o = 1 updates g (line 6).
@@ -1572,6 +1580,7 @@ static int solve_core(pins_workspace *ws, const pins_problem *pb, const pins_par
     EvalOut cur;
     CertOut cert;
     int cert_k = -1, next_cert = 8, n_certs = 0;
+    const bool cert_trace = getenv("PINS_CERT_TRACE") != nullptr;
     bool halving_seen = false;
     FILE *trace = nullptr;
     if (const char *tp = getenv("PINS_TRACE")) trace = fopen(tp, "w");
@@ -1649,6 +1658,10 @@ static int solve_core(pins_workspace *ws, const pins_problem *pb, const pins_par
                 PINS_TRY(certify(ws, pb, phi, psi, s, f, g, cur, false, &cert, st, target));
                 cert_k = k;
                 ++n_certs;
+                if (cert_trace)     // dev instrumentation (PINS_CERT_TRACE=1)
+                    fprintf(stderr, "cert k %d obj %.17g dobj %.17g relgap %.3e primal %.3e tree %d used_tree %d nnz %lld\n",
+                            k, cert.pobj, cert.dobj, cert.gap / std::fabs(cert.pobj), cert.primal, cert.tree_edges,
+                            cert.used_tree, cert.nnz);
                 if (cert.gap <= target) stop = true;
                 else next_cert = k + 1 + std::max(8, (k + 1) / 8);
             }

@@ -115,10 +115,23 @@ struct PassArgs {
     const double *sink_tol;         // LSE: device copy of the tolerance, may be NULL
     int *ctl;                       // LSE control: [0] done flag, [1] sweeps done, [2] rollback
     int check_done;                 // LSE: exit immediately when ctl[0] is set
+    int count_surv;                 // profiling: add the entries evaluated in phase 2 to g_surv
     int count_sweep;                // LSE col pass: ++ctl[1]
     int test_tol;                   // LSE row pass: set done (and rollback) when res <= tol
     const double *a_dot, *f_dot, *b_dot, *g_dot;   // SUM: <a,f> + <b,g> (global finalize)
 };
+
+// Profiling counters (pins_prof_read_work): entries evaluated in phase 2 (the
+// survivors of the skip test), [0] half-sweeps, [1] sum passes.
+__device__ unsigned long long g_surv[2];
+
+__device__ __forceinline__ void count_survivors(int on, int slot, int nsurv) {
+    if (!on) return;
+    unsigned long long v = (unsigned long long)nsurv;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(g_surv + slot, v);
+}
 
 // Conservative fp32 form of the skip test  x = q - w D > thr  (phase 1 of a chunk):
 // qs = q rounded up by 2^-20 |q|, w_lo = w (1 - 2^-19), thr_lo = thr - 2^-20 |thr|;
@@ -760,6 +773,7 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A) {
         }
     }
     float *dsc = dscr + tid * (kCC + 1);       // PC_SQTC: this thread's chunk distances
+    int nsurv = 0;
     const float thr0 = thr_lo_of(mx - kLseCut);
     const SkipCtx sk = skip_setup(P, rb, sp, i, valid, jb, thr0, w_lo, red);
     const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, 0, false, bufs, &tcs, sk,
@@ -772,6 +786,7 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A) {
         if (valid)
             mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx);
         if (sk.kind == 2) record_cert(sk, j0, vmx, thr0, valid);
+        nsurv += __popc(mask);
         if (!valid) return;
         if constexpr (COST == PC_SQTC) {
             // distances are needed only where some lane of the warp has a survivor
@@ -798,6 +813,7 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A) {
     });
     if constexpr (COST == PC_SQTC) tc_teardown(tcs);
     skip_count(P, sk, nskip, jb, je);
+    count_survivors(A.count_surv, 0, nsurv);
     if (valid) {
         P.pa[(long long)sp * P.M + i] = mx;
         P.pb[(long long)sp * P.M + i] = sm;
@@ -894,6 +910,7 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
     int cnt = 0;
     const long long bufbase = (i * P.S + sp) * P.cap;
     float *dsc = dscr + tid * (kCC + 1);
+    int nsurv = 0;
     const SkipCtx sk = skip_setup(P, rb, sp, i, valid, jb, thr32, w_lo, red);
     const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, P.m1_row ? 0 : 1, trial, bufs, &tcs, sk,
                              [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
@@ -903,6 +920,7 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
         if (valid)
             mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx);
         if (sk.kind == 2) record_cert(sk, j0, vmx, thr32, valid);
+        nsurv += __popc(mask);
         if (!valid) return;
         if constexpr (COST == PC_SQTC) {
             // distances are needed only where some lane of the warp has a survivor
@@ -937,6 +955,7 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
     });
     if constexpr (COST == PC_SQTC) tc_teardown(tcs);
     skip_count(P, sk, nskip, jb, je);
+    count_survivors(A.count_surv, 1, nsurv);
     if (valid) {
         P.pa[(long long)sp * P.M + i] = acc;
         if (sparse) P.cnt[i * P.S + sp] = cnt;
