@@ -26,10 +26,21 @@ each a plain definition:
 2. tree duals: the unique (per component, gauge z_root = 0) solution of
    u_i + v_j = C_ij on the edges of T -- the complementary-slackness
    equations of the basis (network-simplex duals of that basis).
-3. c-transforms: u'_i = min_j (C_ij - v_j), then v'_j = min_i (C_ij - u'_i).
+3. component gauges: a disconnected support leaves one free gauge (u + d_A,
+   v - d_A) per component A; the shifts must satisfy d_A - d_B <= R_AB =
+   min_{i in A, j in B} (C_ij - u_i - v_j), a system of difference
+   constraints solved by shortest paths (Bellman-Ford from a virtual source).
+   With balanced components (no optimal flow between them) every feasible
+   choice gives the same bound.
+4. c-transforms: u'_i = min_j (C_ij - v_j), then v'_j = min_i (C_ij - u'_i).
    (u', v') is dual feasible by construction; if T is an optimal basis, its
    duals already are, and the c-transforms change nothing (each row / column
    has a tight tree edge), so <a,u'> + <b,v'> = LP*.
+5. repair (up to 3 forests): support edges that the tree duals violate
+   (C_ij - u_i - v_j < -1e-13 (1 + |<C,X>|)) are forced into the next forest
+   (weight 4 > any plan entry, so the forest drops the lightest edge of the
+   cycle each closes); every forest's bound is valid, the best is kept.
+Finally the entropic duals, c-transformed, are a second candidate.
 """
 from __future__ import annotations
 
@@ -96,6 +107,56 @@ def tree_duals(C: np.ndarray, edges, m: int, n: int) -> Tuple[np.ndarray, np.nda
     return z[:m].copy(), -z[m:]
 
 
+def components(edges, m: int, n: int) -> np.ndarray:
+    """Component label (smallest node index) of every node of the forest."""
+    parent = list(range(m + n))
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+    for i, j, _ in edges:
+        a, b = find(i), find(m + j)
+        if a != b:
+            parent[max(a, b)] = min(a, b)
+    return np.array([find(x) for x in range(m + n)])
+
+
+def component_shift(C: np.ndarray, u: np.ndarray, v: np.ndarray, comp: np.ndarray):
+    """Shortest-path gauge shifts of the components (step 3): constraints d_A - d_B <= R_AB
+    for rows of A and columns of B; Bellman-Ford from a virtual source (d = 0 for all);
+    returns the shifted (u + d_A(i), v - d_B(j)), or (u, v) unchanged if there is one
+    component or a negative cycle."""
+    m, n = C.shape
+    labels = sorted(set(comp.tolist()))
+    K = len(labels)
+    if K <= 1:
+        return u, v
+    idx = {c: k for k, c in enumerate(labels)}
+    A = np.array([idx[c] for c in comp[:m]])
+    B = np.array([idx[c] for c in comp[m:]])
+    r = C - u[:, None] - v[None, :]
+    R = np.full((K, K), np.inf)
+    for a_ in range(K):
+        for b_ in range(K):
+            if a_ != b_:
+                blk = r[np.ix_(A == a_, B == b_)]
+                if blk.size:
+                    R[a_, b_] = blk.min()
+    d = np.zeros(K)
+    for _ in range(K + 1):
+        changed = False
+        for a_ in range(K):
+            for b_ in range(K):
+                if a_ != b_ and np.isfinite(R[a_, b_]) and d[b_] + R[a_, b_] < d[a_]:
+                    d[a_] = d[b_] + R[a_, b_]
+                    changed = True
+        if not changed:
+            return u + d[A], v - d[B]
+    return u, v
+
+
 def ctransform_rows(C: np.ndarray, v: np.ndarray) -> np.ndarray:
     """u_i = min_j (C_ij - v_j): the largest u with u_i + v_j <= C_ij for all j."""
     return (C - v[None, :]).min(axis=1)
@@ -106,14 +167,16 @@ def ctransform_cols(C: np.ndarray, u: np.ndarray) -> np.ndarray:
     return (C - u[:, None]).min(axis=0)
 
 
-def certify(C: np.ndarray, a: np.ndarray, b: np.ndarray, X: np.ndarray, tau: float, duals0=None) -> Dict:
-    """LP KKT of the plan X (reading R11): basis forest of {X >= tau}, tree duals,
-    row then column c-transform.  Returns u, v (dual feasible), dual_obj = <a,u>+<b,v>
-    (<= LP*), primal = ||Xe-a||_1 + ||X^Te-b||_1, pobj = <C,X>, gap = pobj - dual_obj,
-    dual_inf = max(0, max_ij u_i + v_j - C_ij), the forest and how many rows / columns
-    the c-transforms changed (0, 0 when the forest is an optimal basis).
-    duals0 = (u0, v0) replaces the tree duals as the c-transforms' starting point
-    (the entropic-duals candidate of reading R11)."""
+def certify(C: np.ndarray, a: np.ndarray, b: np.ndarray, X: np.ndarray, tau: float, duals0=None,
+            repairs: int = 3) -> Dict:
+    """LP KKT of the plan X (reading R11): basis forests of {X >= tau} (with up to
+    `repairs` forests, step 5), tree duals, component gauges, row then column
+    c-transforms, and the entropic candidate duals0 = (u0, v0) if given; the largest
+    certified bound wins.  Returns u, v (dual feasible), dual_obj = <a,u>+<b,v> (<= LP*),
+    primal = ||Xe-a||_1 + ||X^Te-b||_1, pobj = <C,X>, gap = pobj - dual_obj,
+    dual_inf = max(0, max_ij u_i + v_j - C_ij), the first forest, the tree duals of the
+    best forest (u_tree, v_tree), the number of forests tried and of components, and
+    how many rows / columns the winning c-transform changed."""
     m, n = C.shape
     mask = X >= tau
     rows, cols = np.nonzero(mask)
@@ -121,16 +184,46 @@ def certify(C: np.ndarray, a: np.ndarray, b: np.ndarray, X: np.ndarray, tau: flo
     np.add.at(rowptr, rows + 1, 1)
     rowptr = np.cumsum(rowptr)
     val = X[rows, cols]
-    forest = max_spanning_forest(rowptr, cols, val, m, n)
-    u0, v0 = tree_duals(C, forest, m, n) if duals0 is None else duals0
-    u = ctransform_rows(C, v0)
-    v = ctransform_cols(C, u)
-    dual_obj = float(a @ u + b @ v)
     pobj = float((C * X).sum())
     primal = float(np.abs(X.sum(1) - a).sum() + np.abs(X.sum(0) - b).sum())
+    best = None
+    first_forest = None
+    forced = np.zeros(len(val), dtype=bool)
+    tol_rc = 1e-13 * (1.0 + abs(pobj))
+    rounds = 0
+    ncomp = 0
+    for rnd in range(repairs):
+        w = np.where(forced, 4.0, val)
+        forest = max_spanning_forest(rowptr, cols, w, m, n)
+        if first_forest is None:
+            first_forest = forest
+        u0, v0 = tree_duals(C, forest, m, n)
+        comp = components(forest, m, n)
+        ncomp = len(set(comp.tolist()))
+        u0, v0 = component_shift(C, u0, v0, comp)
+        u = ctransform_rows(C, v0)
+        v = ctransform_cols(C, u)
+        D = float(a @ u + b @ v)
+        rounds = rnd + 1
+        if best is None or D > best[0]:
+            best = (D, u, v, u0, v0, 1)
+        if rnd + 1 == repairs:
+            break
+        viol = (C[rows, cols] - u0[rows] - v0[cols]) < -tol_rc
+        if not viol.any():
+            break
+        forced |= viol
+    if duals0 is not None:
+        u = ctransform_rows(C, duals0[1])
+        v = ctransform_cols(C, u)
+        D = float(a @ u + b @ v)
+        if D > best[0]:
+            best = (D, u, v, duals0[0], duals0[1], 0)
+    dual_obj, u, v, u0, v0, used_tree = best
     dual_inf = float(max(0.0, (u[:, None] + v[None, :] - C).max()))
     tol = 1e-12 * (1.0 + float(np.abs(C).max()))          # "changed" beyond rounding
-    return dict(u=u, v=v, u_tree=u0, v_tree=v0, forest=forest, dual_obj=dual_obj, pobj=pobj,
-                primal=primal, gap=pobj - dual_obj, dual_inf=dual_inf,
+    return dict(u=u, v=v, u_tree=u0, v_tree=v0, forest=first_forest, dual_obj=dual_obj, pobj=pobj,
+                primal=primal, gap=pobj - dual_obj, dual_inf=dual_inf, used_tree=used_tree,
+                forests=rounds, components=ncomp,
                 rows_changed=int(np.count_nonzero(np.abs(u - u0) > tol)),
                 cols_changed=int(np.count_nonzero(np.abs(v - v0) > tol)))

@@ -190,6 +190,7 @@ struct pins_workspace {
     TreeArgs tree_last;                // arguments of the last tree build (certificate replay)
     // LP certificate (pins_cert.cuh): tree-dual scratch, c-transform partials, candidates
     DevBuf cz, cdd, cdf, ctc, cpart, cu0, cv0, cu1, cv1, cbu, cbv, crow;
+    DevBuf ccomp, ccid, cinfo, cR, cdsh, cw;
     bool csr_ready = false, csc_ready = false;
     bool x0_enable = false;    // solve_core: warm-start the cluster tree-PCG from the previous direction
     bool dir_valid = false;    // ws->dir holds the previous Newton system's solution
@@ -900,7 +901,8 @@ bool use_tree_cg(pins_workspace *ws, long long m, long long n) {
 
 int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const double *rhs, double *x,
                 double rtol, int maxit, const double *gradf, const double *gradg, const double *a,
-                const double *b, cudaStream_t st, int setup_only = 0, bool force_rebuild = false) {
+                const double *b, cudaStream_t st, int setup_only = 0, bool force_rebuild = false,
+                const double *wval = nullptr) {
     const long long N = m + n, nnz = std::max<long long>(ws->nnz, 1);
     PINS_TRY(ensure(ws->cgst, sizeof(double) * 16));
     // persistent arrays first, nnz-sized scratch last (offsets stay put as nnz changes)
@@ -921,7 +923,7 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     A.nnz = ws->nnz;
     A.rowptr = ptr<long long>(ws->rowptr);
     A.colidx = ptr<int>(ws->colidx);
-    A.val = ptr<double>(ws->val);
+    A.val = wval ? wval : ptr<double>(ws->val);     // wval: certificate repair weights (setup only)
     A.colptr = ptr<long long>(ws->colptr);
     A.rowidx = ptr<int>(ws->rowidx);
     A.valT = ptr<double>(ws->valT);
@@ -1085,7 +1087,7 @@ int ctrans(pins_workspace *ws, const pins_problem *pb, int orient, int mode, con
 
 struct CertOut {
     double primal = 0, pobj = 0, dobj = -INFINITY, gap = INFINITY, dual_inf = -1;
-    int tree_edges = 0, used_tree = 0;
+    int tree_edges = 0, used_tree = 0, components = 0, repairs = 0, violations = 0;
     long long nnz = 0;
 };
 
@@ -1112,6 +1114,92 @@ int measure_dual_inf(pins_workspace *ws, const pins_problem *pb, CertOut *co, cu
     return PINS_OK;
 }
 
+// c-transforms of (u0, v0) (rows, then columns) into (u1, v1), bound D; the
+// best bound so far and its duals are kept in co / ws->cbu, cbv.
+int ctrans_candidate(pins_workspace *ws, const pins_problem *pb, const double *v0, double *u1, double *v1,
+                     int used_tree, CertOut *co, cudaStream_t st) {
+    PINS_TRY(ctrans(ws, pb, 0, 0, v0, nullptr, u1, st));      // u'_i = min_j C_ij - v_j
+    PINS_TRY(ctrans(ws, pb, 1, 0, u1, nullptr, v1, st));      // v'_j = min_i C_ij - u'_i
+    double D = 0.0;
+    PINS_TRY(dual_value(ws, pb, u1, v1, &D, st));
+    if (std::isfinite(D) && D > co->dobj) {
+        co->dobj = D;
+        co->used_tree = used_tree;
+        PINS_CUDA(cudaMemcpyAsync(ws->cbu.p, u1, sizeof(double) * pb->m, cudaMemcpyDeviceToDevice, st));
+        PINS_CUDA(cudaMemcpyAsync(ws->cbv.p, v1, sizeof(double) * pb->n, cudaMemcpyDeviceToDevice, st));
+    }
+    return PINS_OK;
+}
+
+// Tree candidate (reading R11): maximum-weight spanning forest of the support,
+// tree duals, component gauges by shortest paths, c-transforms; then up to
+// kRepairRounds repairs: support edges the tree duals violate are forced into
+// the next forest (pins_cert.cuh support_rc_kernel).
+constexpr int kRepairRounds = 3;
+int certify_tree(pins_workspace *ws, const pins_problem *pb, const EvalOut &cur, CertOut *co, cudaStream_t st,
+                 double target_gap) {
+    const long long m = pb->m, n = pb->n, N = m + n, nnz = ws->nnz;
+    for (DevBuf *b : {&ws->cz, &ws->cdd, &ws->cdf, &ws->ctc}) PINS_TRY(ensure(*b, sizeof(double) * N));
+    PINS_TRY(ensure(ws->ccomp, sizeof(int) * N));
+    PINS_TRY(ensure(ws->ccid, sizeof(int) * N));
+    PINS_TRY(ensure(ws->cinfo, sizeof(int) * 8));
+    PINS_TRY(ensure(ws->cR, sizeof(unsigned long long) * kMaxComp * kMaxComp));
+    PINS_TRY(ensure(ws->cdsh, sizeof(double) * kMaxComp));
+    PINS_TRY(ensure(ws->cw, sizeof(double) * std::max<long long>(nnz, 1)));
+    double *u0 = ptr<double>(ws->cu0), *v0 = ptr<double>(ws->cv0);
+    double *u1 = ptr<double>(ws->cu1), *v1 = ptr<double>(ws->cv1);
+    int *info = ptr<int>(ws->cinfo);
+    const CostDesc cd = make_cd(pb);
+    const double *wts = nullptr;                    // round 0: the plan's own weights
+    for (int round = 0; round < kRepairRounds; ++round) {
+        PINS_TRY(run_cg_tree(ws, m, n, 0.0, ptr<double>(ws->rhs), ptr<double>(ws->uv), 0.5, 1, nullptr, nullptr,
+                             nullptr, nullptr, st, 1, true, wts));
+        const TreeArgs &T = ws->tree_last;
+        TreeDualArgs D;
+        D.m = (int)m; D.n = (int)n;
+        D.ctr = T.ctr; D.rstart = T.rstart;
+        D.fu = T.fu; D.fv1 = T.fv1; D.fv2 = T.fv2; D.fs1 = T.fs1; D.fs2 = T.fs2;
+        D.tei = T.tei; D.tej = T.tej;
+        D.cd = cd;
+        D.scale = pb->cost_scale;
+        D.dd = ptr<double>(ws->cdd); D.df = ptr<double>(ws->cdf); D.tc = ptr<double>(ws->ctc);
+        D.z = ptr<double>(ws->cz);
+        D.comp = ptr<int>(ws->ccomp);
+        LAUNCH(PINS_PROF_VEC, st, tree_duals_kernel<<<1, 1024, 0, st>>>(D));
+        LAUNCH(PINS_PROF_VEC, st, split_duals_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(m, n, D.z, u0, v0));
+        // component gauges (no-ops on the device when the forest is connected)
+        unsigned long long *R = ptr<unsigned long long>(ws->cR);
+        LAUNCH(PINS_PROF_VEC, st, comp_ids_kernel<<<1, 1024, 0, st>>>((int)N, D.comp, ptr<int>(ws->ccid), info, R));
+        LAUNCH(PINS_PROF_VEC, st, comp_rmin_kernel<<<(int)((m + kCtT - 1) / kCtT), kCtT, 0, st>>>(
+            m, n, cd, pb->cost_scale, u0, v0, D.comp, ptr<int>(ws->ccid), info, R));
+        LAUNCH(PINS_PROF_VEC, st, comp_shift_solve_kernel<<<1, 1, 0, st>>>(info, R, ptr<double>(ws->cdsh), info + 1));
+        LAUNCH(PINS_PROF_VEC, st, comp_shift_apply_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(
+            m, n, D.comp, ptr<int>(ws->ccid), info + 1, ptr<double>(ws->cdsh), u0, v0));
+        PINS_CUDA(cudaGetLastError());
+        PINS_TRY(ctrans_candidate(ws, pb, v0, u1, v1, 1, co, st));
+        int hi[4];
+        PINS_CUDA(cudaMemcpyAsync(hi, info, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
+        PINS_CUDA(cudaMemcpyAsync(hi + 2, T.ctr + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+        PINS_CUDA(cudaStreamSynchronize(st));
+        co->tree_edges = hi[2];
+        co->components = hi[0];
+        co->repairs = round;
+        if (co->pobj - co->dobj <= target_gap || round + 1 == kRepairRounds) break;
+        // repair: force the support edges these duals violate into the next forest
+        PINS_CUDA(cudaMemsetAsync(info + 2, 0, sizeof(int), st));
+        LAUNCH(PINS_PROF_VEC, st, support_rc_kernel<<<grid_1d(nnz, ws->nsm), 256, 0, st>>>(
+            nnz, T.erow, ptr<int>(ws->colidx), ptr<double>(ws->val), cd, pb->cost_scale, u0, v0,
+            1e-13 * (1.0 + std::fabs(cur.cost)), ptr<double>(ws->cw), round == 0 ? 1 : 0, info + 2));
+        int nviol = 0;
+        PINS_CUDA(cudaMemcpyAsync(&nviol, info + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+        PINS_CUDA(cudaStreamSynchronize(st));
+        co->violations = nviol;
+        if (nviol == 0) break;
+        wts = ptr<double>(ws->cw);
+    }
+    return PINS_OK;
+}
+
 // Certificate of the plan X~(f, g) at centre (phi, psi, s), whose evaluation
 // (sums, CSR / CSC at tau) is the workspace state `cur` (reading R11): basis
 // forest -> tree duals -> row / column c-transforms; the entropic duals
@@ -1131,44 +1219,17 @@ int certify(pins_workspace *ws, const pins_problem *pb, const double *phi, const
     double *u0 = ptr<double>(ws->cu0), *v0 = ptr<double>(ws->cv0);
     double *u1 = ptr<double>(ws->cu1), *v1 = ptr<double>(ws->cv1);
     for (int cand = 0; cand < 2; ++cand) {
-        if (cand == 0) {                            // tree duals of the basis forest
+        if (cand == 0) {                            // tree duals of the basis forest, repaired
             if (!(N <= kTreeMaxNodes && ws->csr_ready && ws->csc_ready && ws->nnz >= 1)) continue;
-            PINS_TRY(run_cg_tree(ws, m, n, 0.0, ptr<double>(ws->rhs), ptr<double>(ws->uv), 0.5, 1, nullptr,
-                                 nullptr, nullptr, nullptr, st, 1, true));
-            for (DevBuf *b : {&ws->cz, &ws->cdd, &ws->cdf, &ws->ctc}) PINS_TRY(ensure(*b, sizeof(double) * N));
-            const TreeArgs &T = ws->tree_last;
-            TreeDualArgs D;
-            D.m = (int)m; D.n = (int)n;
-            D.ctr = T.ctr; D.rstart = T.rstart;
-            D.fu = T.fu; D.fv1 = T.fv1; D.fv2 = T.fv2; D.fs1 = T.fs1; D.fs2 = T.fs2;
-            D.tei = T.tei; D.tej = T.tej;
-            D.cd = make_cd(pb);
-            D.scale = pb->cost_scale;
-            D.dd = ptr<double>(ws->cdd); D.df = ptr<double>(ws->cdf); D.tc = ptr<double>(ws->ctc);
-            D.z = ptr<double>(ws->cz);
-            LAUNCH(PINS_PROF_VEC, st, tree_duals_kernel<<<1, 1024, 0, st>>>(D));
-            LAUNCH(PINS_PROF_VEC, st, split_duals_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(m, n, D.z, u0, v0));
-            PINS_CUDA(cudaGetLastError());
-            int te = 0;
-            PINS_CUDA(cudaMemcpyAsync(&te, T.ctr + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
-            PINS_CUDA(cudaStreamSynchronize(st));
-            co->tree_edges = te;
-        } else {                                    // entropic duals (reading R8)
+            PINS_TRY(certify_tree(ws, pb, cur, co, st, target_gap));
+            if (co->pobj - co->dobj <= target_gap) break;
+            continue;
+        } else {            // entropic duals (reading R8)
             LAUNCH(PINS_PROF_VEC, st, lp_duals_kernel<<<grid_1d(N, ws->nsm), 256, 0, st>>>(
                 m, n, pb->eta, 1.0 / s, f, g, phi, psi, u0, v0));
             PINS_CUDA(cudaGetLastError());
         }
-        PINS_TRY(ctrans(ws, pb, 0, 0, v0, nullptr, u1, st));      // u'_i = min_j C_ij - v_j
-        PINS_TRY(ctrans(ws, pb, 1, 0, u1, nullptr, v1, st));      // v'_j = min_i C_ij - u'_i
-        double D = 0.0;
-        PINS_TRY(dual_value(ws, pb, u1, v1, &D, st));
-        if (std::isfinite(D) && D > co->dobj) {
-            co->dobj = D;
-            co->used_tree = cand == 0 ? 1 : 0;
-            PINS_CUDA(cudaMemcpyAsync(ws->cbu.p, u1, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
-            PINS_CUDA(cudaMemcpyAsync(ws->cbv.p, v1, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-        }
-        if (co->pobj - co->dobj <= target_gap) break;   // the basis duals already certify the target
+        PINS_TRY(ctrans_candidate(ws, pb, v0, u1, v1, 0, co, st));
     }
     co->gap = co->pobj - co->dobj;
     if (want_dual_inf) PINS_TRY(measure_dual_inf(ws, pb, co, st));
@@ -1579,7 +1640,7 @@ static int solve_core(pins_workspace *ws, const pins_problem *pb, const pins_par
     bool converged = false;
     EvalOut cur;
     CertOut cert;
-    int cert_k = -1, next_cert = 8, n_certs = 0;
+    int cert_k = -1, next_cert = 0, n_certs = 0;
     const bool cert_trace = getenv("PINS_CERT_TRACE") != nullptr;
     bool halving_seen = false;
     FILE *trace = nullptr;
@@ -1651,7 +1712,8 @@ static int solve_core(pins_workspace *ws, const pins_problem *pb, const pins_par
             pins_params p1 = *prm;
             p1.outer_rule = 1;
             const bool halving = outer_converged(objs, &p1);
-            const bool trigger = k + 1 >= next_cert || (halving && !halving_seen);
+            // first attempt when the halving estimator first fires, then every max(8, k/16)
+            const bool trigger = (halving && !halving_seen) || (halving_seen && k + 1 >= next_cert);
             halving_seen = halving_seen || halving;
             if (trigger && cur.gnorm <= prm->newton_tol) {
                 const double target = prm->outer_tol * std::fabs(cur.cost);
@@ -1659,11 +1721,12 @@ static int solve_core(pins_workspace *ws, const pins_problem *pb, const pins_par
                 cert_k = k;
                 ++n_certs;
                 if (cert_trace)     // dev instrumentation (PINS_CERT_TRACE=1)
-                    fprintf(stderr, "cert k %d obj %.17g dobj %.17g relgap %.3e primal %.3e tree %d used_tree %d nnz %lld\n",
+                    fprintf(stderr, "cert k %d obj %.17g dobj %.17g relgap %.3e primal %.3e tree %d comps %d "
+                            "repairs %d viol %d used_tree %d nnz %lld\n",
                             k, cert.pobj, cert.dobj, cert.gap / std::fabs(cert.pobj), cert.primal, cert.tree_edges,
-                            cert.used_tree, cert.nnz);
+                            cert.components, cert.repairs, cert.violations, cert.used_tree, cert.nnz);
                 if (cert.gap <= target) stop = true;
-                else next_cert = k + 1 + std::max(8, (k + 1) / 8);
+                else next_cert = k + 1 + std::max(8, (k + 1) / 16);
             }
         } else {
             stop = outer_converged(objs, prm);

@@ -26,6 +26,9 @@
 
 namespace pins {
 
+constexpr int kCtT = 128;              // threads of the c-transform / component passes
+constexpr int kCtC = 32;               // staged pass columns per chunk (points)
+
 struct TreeDualArgs {
     int m, n;
     const int *ctr;                    // [1] rounds, [2] tree edges
@@ -38,6 +41,7 @@ struct TreeDualArgs {
     double *df;                        // [N] per record: fill payload d2 - d1 (z_v1 - z_v2)
     double *tc;                        // [N] per tree edge: C_ij
     double *z;                         // [N] output: z = (u, -v)
+    int *comp;                         // [N] output: component root of each node
 };
 
 __device__ __forceinline__ double cost_entry(const CostDesc &cd, double scale, long long i, long long j) {
@@ -82,13 +86,140 @@ __global__ void __launch_bounds__(1024, 1) tree_duals_kernel(TreeDualArgs A) {
         }
         __syncthreads();
     }
+    for (int v = tid; v < N; v += blockDim.x) A.comp[v] = v;    // never eliminated: own root
+    __syncthreads();
     for (int r = nr - 1; r >= 0; --r) {             // backward: z_u = z_v1 + d1
         const int q1 = A.rstart[r + 1];
         for (int q = A.rstart[r] + tid; q < q1; q += blockDim.x) {
-            const int v1 = A.fv1[q];
-            A.z[A.fu[q]] = v1 >= 0 ? A.z[v1] + A.dd[q] : 0.0;
+            const int v1 = A.fv1[q], u = A.fu[q];
+            A.z[u] = v1 >= 0 ? A.z[v1] + A.dd[q] : 0.0;
+            A.comp[u] = v1 >= 0 ? A.comp[v1] : u;
         }
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------------- basis repair (R11)
+// Reduced costs of the support edges under the tree duals: an edge with
+// C_ij - u_i - v_j < -tol violates dual feasibility; it is forced into the
+// next forest (weight 4 > any plan entry), so the next maximum spanning forest
+// drops the lightest edge of the cycle it closes (a dual-simplex-like pivot).
+// Forced edges stay forced.  cnt[0] += violations.
+__global__ void support_rc_kernel(long long nnz, const int *erow, const int *colidx, const double *val,
+                                  CostDesc cd, double scale, const double *u, const double *v, double tol,
+                                  double *w, int first, int *cnt) {
+    int nv = 0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int i = erow[e], j = colidx[e];
+        const double r = cost_entry(cd, scale, i, j) - u[i] - v[j];
+        const bool viol = r < -tol;
+        nv += viol ? 1 : 0;
+        const bool forced = !first && w[e] == 4.0;
+        w[e] = (viol || forced) ? 4.0 : val[e];
+    }
+    nv = warp_sum_int(nv);
+    if ((threadIdx.x & 31) == 0 && nv) atomicAdd(cnt, nv);
+}
+
+// ------------------------------------------------- component gauges (R11)
+// A disconnected support leaves one free gauge per component (u + d, v - d).
+// The shifts d_A must satisfy d_A - d_B <= R_AB = min_{i in A, j in B}
+// (C_ij - u_i - v_j) (rows of A, columns of B); with balanced components
+// (no optimal flow between them) every feasible choice gives the same bound,
+// and shortest-path distances are one.  ncomp <= kMaxComp.
+constexpr int kMaxComp = 64;
+
+__device__ __forceinline__ unsigned long long ord_key(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+// one CTA: component ids (roots -> 0..K-1), K in cid_info[0] (-1 if > kMaxComp)
+__global__ void __launch_bounds__(1024) comp_ids_kernel(int N, const int *comp, int *cid, int *cid_info,
+                                                        unsigned long long *R) {
+    __shared__ int cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    for (int x = threadIdx.x; x < N; x += blockDim.x)
+        if (comp[x] == x) cid[x] = atomicAdd(&cnt, 1);        // any numbering works (shortest paths)
+    __syncthreads();
+    if (threadIdx.x == 0) cid_info[0] = cnt <= kMaxComp ? cnt : -1;
+    for (int t = threadIdx.x; t < kMaxComp * kMaxComp; t += blockDim.x) R[t] = ~0ull;
+}
+
+// R_AB over all pairs (i, j) in different components: thread per row, columns staged
+__global__ void __launch_bounds__(kCtT) comp_rmin_kernel(long long m, long long n, CostDesc cd, double scale,
+                                                         const double *u, const double *v, const int *comp,
+                                                         const int *cid, const int *cid_info,
+                                                         unsigned long long *R) {
+    __shared__ unsigned long long Rs[kMaxComp * kMaxComp];
+    __shared__ int cc[256];
+    __shared__ double vs[256];
+    const int K = cid_info[0];
+    if (K <= 1) return;
+    for (int t = threadIdx.x; t < K * K; t += blockDim.x) Rs[t] = ~0ull;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const bool valid = i < m;
+    const int A = valid ? cid[comp[i]] : 0;
+    const double ui = valid ? u[i] : 0.0;
+    for (long long j0 = 0; j0 < n; j0 += 256) {
+        const int nc = (int)min(256LL, n - j0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+            cc[t] = cid[comp[m + j0 + t]];
+            vs[t] = v[j0 + t];
+        }
+        __syncthreads();
+        if (!valid) continue;
+        for (int c = 0; c < nc; ++c) {
+            const int B = cc[c];
+            if (B == A) continue;
+            const double r = cost_entry(cd, scale, i, j0 + c) - ui - vs[c];
+            atomicMin(Rs + A * K + B, ord_key(r));
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < K * K; t += blockDim.x)
+        if (Rs[t] != ~0ull) atomicMin(R + t, Rs[t]);
+}
+
+// one thread: Bellman-Ford from a virtual source (d = 0 for all), edges B -> A of
+// weight R_AB (d_A <= d_B + R_AB); then shift u_i += d_{A(i)}, v_j -= d_{B(j)}.
+// A negative cycle (no feasible shifts) leaves the duals unshifted.
+__global__ void comp_shift_solve_kernel(const int *cid_info, const unsigned long long *R, double *dsh, int *ok) {
+    const int K = cid_info[0];
+    *ok = 0;
+    if (K <= 1) return;
+    double d[kMaxComp];
+    for (int a = 0; a < K; ++a) d[a] = 0.0;
+    bool changed = true;
+    for (int it = 0; it <= K && changed; ++it) {
+        changed = false;
+        for (int a = 0; a < K; ++a)
+            for (int b = 0; b < K; ++b) {
+                const unsigned long long key = R[a * K + b];
+                if (a == b || key == ~0ull) continue;
+                const double nd = d[b] + ord_val(key);
+                if (nd < d[a]) { d[a] = nd; changed = true; }
+            }
+    }
+    if (changed) return;                             // negative cycle
+    for (int a = 0; a < K; ++a) dsh[a] = d[a];
+    *ok = 1;
+}
+
+__global__ void comp_shift_apply_kernel(long long m, long long n, const int *comp, const int *cid, const int *ok,
+                                        const double *dsh, double *u, double *v) {
+    if (!*ok) return;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < m + n;
+         k += (long long)gridDim.x * blockDim.x) {
+        const double d = dsh[cid[comp[k]]];
+        if (k < m) u[k] += d;
+        else v[k - m] -= d;
     }
 }
 
@@ -116,8 +247,6 @@ struct CtArgs {
     double *part;                      // [S * M]
 };
 
-constexpr int kCtT = 128;
-constexpr int kCtC = 32;               // staged pass columns per chunk (points)
 
 __device__ __forceinline__ double ct_fold(int mode, double acc, double v) {
     return mode == 0 ? fmin(acc, v) : fmax(acc, v);

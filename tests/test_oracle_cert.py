@@ -165,3 +165,51 @@ def test_certificate_on_a_degenerate_assignment_is_a_valid_bound():
     cert = lc.certify(C, a, b, X, tau=0.0)
     assert cert["dual_obj"] <= opt + 1e-14
     assert cert["dual_inf"] <= 1e-15
+
+
+def test_component_gauges_make_a_disconnected_support_exact():
+    # two balanced blocks with expensive cross costs: the optimal plan has no flow
+    # between them, so the support (and the forest) has two components whose tree
+    # duals carry arbitrary relative gauges; the shortest-path shifts (step 3) make
+    # them feasible and the bound exact
+    rng = np.random.default_rng(31)
+    C = 1.0 + rng.random((6, 6))
+    C[:3, :3] = rng.random((3, 3))
+    C[3:, 3:] = rng.random((3, 3))
+    a = norm(np.array([1.0, 2.0, 3.0, 1.5, 2.5, 2.0]))
+    b = norm(np.array([2.0, 1.0, 3.0, 2.0, 2.0, 2.0]))
+    assert abs(a[:3].sum() - b[:3].sum()) < 1e-15        # balanced blocks
+    ex = solve_exact(C, a, b)
+    X = ex["X"]
+    assert np.all(X[:3, 3:] == 0) and np.all(X[3:, :3] == 0)
+    cert = lc.certify(C, a, b, X, tau=1e-300)
+    assert cert["components"] >= 2
+    assert cert["dual_obj"] == pytest.approx(ex["obj"], rel=1e-13)
+    assert cert["dual_inf"] <= 1e-15
+    # the shifts alone restore feasibility of the tree duals (before any c-transform)
+    forest = lc.max_spanning_forest(*csr(X >= 1e-300, X), 6, 6)
+    u0, v0 = lc.tree_duals(C, forest, 6, 6)
+    us, vs = lc.component_shift(C, u0, v0, lc.components(forest, 6, 6))
+    assert (us[:, None] + vs[None, :] - C).max() <= 1e-15
+
+
+def test_repair_forces_violated_support_edges_into_the_forest():
+    # a plan whose heaviest spanning forest is not the optimal basis: the tree duals
+    # violate a support edge; forcing it in (step 5) recovers the optimal basis
+    rng = np.random.default_rng(5)
+    m, n = 7, 8
+    C = rng.random((m, n))
+    a, b = norm(rng.random(m) + 0.1), norm(rng.random(n) + 0.1)
+    ex = solve_exact(C, a, b)
+    X = ex["X"].copy()
+    basis = np.argwhere(X > 0)
+    i, j = basis[np.argmin(X[X > 0])]                   # shrink the smallest basic flow ...
+    X[i, j] = 1e-12
+    nb = np.argwhere(ex["X"] == 0)
+    k = nb[0]
+    X[k[0], k[1]] = 1e-6                                # ... below a non-basic entry
+    one = lc.certify(C, a, b, X, tau=1e-300, repairs=1)
+    rep = lc.certify(C, a, b, X, tau=1e-300, repairs=3)
+    assert rep["dual_obj"] >= one["dual_obj"] - 1e-15
+    assert rep["dual_obj"] <= ex["obj"] + 1e-14
+    assert rep["dual_inf"] <= 1e-15
