@@ -21,8 +21,9 @@ if mode in ("sweep", "eval"):
     f = torch.zeros(w.m, dtype=torch.float64, device="cuda")
     g = torch.zeros(w.n, dtype=torch.float64, device="cuda")
     ws = pins.Workspace()
-    for _ in range(30 if mode == "sweep" else 20):
-        pins.sinkhorn_sweep(ws, pb, phi, psi, s, f, g)
+    # one device-side Sinkhorn phase (argmax seeds and chunk-skip certificates carry
+    # across its sweeps, as inside pins_solve)
+    pins.sinkhorn(ws, pb, phi, psi, s, f, g, 0.0, 30 if mode == "sweep" else 20)
     if mode == "eval":
         for _ in range(10):
             pins.evaluate(ws, pb, phi, psi, s, f, g, tau=1e-4 / (w.m * w.n))
