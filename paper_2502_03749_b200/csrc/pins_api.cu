@@ -1,5 +1,7 @@
 // pins_api.cu -- C ABI of libpins_b200.so (include/pins.h): workspace, kernel
 // launchers, the Newton step and the host-driven PINS loop (Algorithm 2).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -178,6 +180,7 @@ struct pins_workspace {
     long long key_m = -1, key_n = -1, key_ldc = -1;
     int key_kind = -1, key_d = -1;
     int cost_row = 0, cost_col = 0, dp = 4, skipk = 0;
+    CUtensorMap tm_row, tm_col;        // dense C staged by TMA (PC_DENSE_*_T)
     int S[2] = {1, 1};
     long long pcap = 16;       // per (row, split) sparsify capacity
     long long m = 0, n = 0, nnz = 0;
@@ -219,6 +222,8 @@ extern "C" void pins_default_params(pins_params *p) {
 extern "C" int pins_workspace_create(pins_workspace **out) {
     PINS_ARG(out != nullptr, "ws");
     pins_workspace *ws = new pins_workspace();
+    memset(&ws->tm_row, 0, sizeof ws->tm_row);
+    memset(&ws->tm_col, 0, sizeof ws->tm_col);
     PINS_CUDA(cudaGetDevice(&ws->dev));
     PINS_CUDA(cudaDeviceGetAttribute(&ws->nsm, cudaDevAttrMultiProcessorCount, ws->dev));
     PINS_CUDA(cudaMallocHost(&ws->h, 64 * sizeof(double)));
@@ -348,6 +353,37 @@ struct EvalOut {
 // Thread-per-row dense passes (pins_pass.cuh).
 int dp_for(int d) { return d <= 4 ? 4 : d <= 12 ? 12 : 16; }
 
+// Tensor maps of a dense C for the TMA-staged passes (pins_pass.cuh): the row
+// orientation loads {16 columns x 128 rows} boxes with the 128-byte swizzle, the
+// column orientation {128 columns x 32 rows} boxes.  Out-of-range elements of a
+// box are zero-filled by the TMA unit (the passes mask them).
+int make_dense_maps(pins_workspace *ws, const pins_problem *pb) {
+    static PFN_cuTensorMapEncodeTiled encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        PINS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        PINS_ARG(fn != nullptr && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)pb->n, (cuuint64_t)pb->m};
+    const cuuint64_t strides[1] = {(cuuint64_t)pb->ldc * sizeof(double)};
+    const cuuint32_t es[2] = {1, 1};
+    const cuuint32_t box_row[2] = {16, (cuuint32_t)kPT};
+    const cuuint32_t box_col[2] = {(cuuint32_t)kPT, (cuuint32_t)kCC};
+    CUresult r1 = encode(&ws->tm_row, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(pb->C), dims, strides,
+                         box_row, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r2 = encode(&ws->tm_col, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(pb->C), dims, strides,
+                         box_col, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) {
+        snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled failed (%d, %d)", (int)r1, (int)r2);
+        return PINS_ERR_CUDA;
+    }
+    return PINS_OK;
+}
+
 // Forget the derived cost data of the previous problem.  Every public entry
 // point that takes a pins_problem calls this first, so a workspace reused with
 // a new problem -- even one whose arrays sit at the old addresses, or whose
@@ -409,6 +445,13 @@ int prepare_pass(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
         ws->cost_col = PC_DENSE_COL;
         ws->skipk = 0;
         ws->dp = 4;
+        // TMA staging needs a 16-byte aligned base and row pitch (else the thread-staged path)
+        const bool aligned = (reinterpret_cast<uintptr_t>(pb->C) & 15) == 0 && (pb->ldc % 2) == 0;
+        if (aligned && getenv("PINS_NO_TMA") == nullptr) {
+            PINS_TRY(make_dense_maps(ws, pb));
+            ws->cost_row = PC_DENSE_ROW_T;
+            ws->cost_col = PC_DENSE_COL_T;
+        }
     } else {
         const int dp = dp_for(pb->d);
         ws->dp = dp;
@@ -545,27 +588,49 @@ void fill_side(pins_workspace *ws, const pins_problem *pb, int o, const double *
         }                                   \
     } while (0)
 
-cudaError_t launch_lse(int cost, int dp, int grid, cudaStream_t st, const PassArgs &A) {
+// dynamic shared memory of a pass kernel instantiation: the TMA ring for dense
+// costs staged by TMA (attribute set once per instantiation), else none
+template <class K>
+size_t pass_smem(K kern, bool tma) {
+    if (!tma) return 0;
+    static bool done = false;
+    if (!done) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+        done = true;
+    }
+    return kTmaSmem;
+}
+#define LSE_LAUNCH(CLS, C_, DP_)                                                                            \
+    LAUNCH(CLS, st, lse_pass_kernel<C_, DP_><<<grid, kPT, pass_smem(lse_pass_kernel<C_, DP_>, kTma<C_>), st>>>(A, tm))
+#define SUM_LAUNCH(C0_, C1_, DP_)                                                                            \
+    LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<C0_, C1_, DP_><<<grid, kPT,                                    \
+           pass_smem(sum_pass_kernel<C0_, C1_, DP_>, kTma<C0_>), st>>>(A, tm0, tm1))
+
+cudaError_t launch_lse(int cost, int dp, int grid, cudaStream_t st, const PassArgs &A, const CUtensorMap &tm) {
     switch (cost) {
-        case PC_DENSE_ROW: LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_DENSE_ROW, 4><<<grid, kPT, 0, st>>>(A)); break;
-        case PC_DENSE_COL: LAUNCH(PINS_PROF_SWEEP_COL, st, lse_pass_kernel<PC_DENSE_COL, 4><<<grid, kPT, 0, st>>>(A)); break;
-        case PC_SQ32: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_SQ32, DP><<<grid, kPT, 0, st>>>(A))); break;
-        case PC_L132: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_L132, DP><<<grid, kPT, 0, st>>>(A))); break;
-        case PC_SQ64: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_SQ64, DP><<<grid, kPT, 0, st>>>(A))); break;
-        case PC_SQTC: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_SQTC, DP><<<grid, kPT, 0, st>>>(A))); break;
-        default: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_pass_kernel<PC_L164, DP><<<grid, kPT, 0, st>>>(A))); break;
+        case PC_DENSE_ROW: LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_DENSE_ROW, 4); break;
+        case PC_DENSE_COL: LSE_LAUNCH(PINS_PROF_SWEEP_COL, PC_DENSE_COL, 4); break;
+        case PC_DENSE_ROW_T: LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_DENSE_ROW_T, 4); break;
+        case PC_DENSE_COL_T: LSE_LAUNCH(PINS_PROF_SWEEP_COL, PC_DENSE_COL_T, 4); break;
+        case PC_SQ32: PINS_DP_DISPATCH(dp, LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_SQ32, DP)); break;
+        case PC_L132: PINS_DP_DISPATCH(dp, LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_L132, DP)); break;
+        case PC_SQ64: PINS_DP_DISPATCH(dp, LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_SQ64, DP)); break;
+        case PC_SQTC: PINS_DP_DISPATCH(dp, LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_SQTC, DP)); break;
+        default: PINS_DP_DISPATCH(dp, LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_L164, DP)); break;
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_sum(int cost, int dp, int grid, cudaStream_t st, const PassArgs &A) {
+cudaError_t launch_sum(int cost, int dp, int grid, cudaStream_t st, const PassArgs &A, const CUtensorMap &tm0,
+                       const CUtensorMap &tm1) {
     switch (cost) {
-        case PC_DENSE_ROW: LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_DENSE_ROW, PC_DENSE_COL, 4><<<grid, kPT, 0, st>>>(A)); break;
-        case PC_SQ32: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_SQ32, PC_SQ32, DP><<<grid, kPT, 0, st>>>(A))); break;
-        case PC_L132: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_L132, PC_L132, DP><<<grid, kPT, 0, st>>>(A))); break;
-        case PC_SQ64: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_SQ64, PC_SQ64, DP><<<grid, kPT, 0, st>>>(A))); break;
-        case PC_SQTC: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_SQTC, PC_SQTC, DP><<<grid, kPT, 0, st>>>(A))); break;
-        default: PINS_DP_DISPATCH(dp, LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<PC_L164, PC_L164, DP><<<grid, kPT, 0, st>>>(A))); break;
+        case PC_DENSE_ROW: SUM_LAUNCH(PC_DENSE_ROW, PC_DENSE_COL, 4); break;
+        case PC_DENSE_ROW_T: SUM_LAUNCH(PC_DENSE_ROW_T, PC_DENSE_COL_T, 4); break;
+        case PC_SQ32: PINS_DP_DISPATCH(dp, SUM_LAUNCH(PC_SQ32, PC_SQ32, DP)); break;
+        case PC_L132: PINS_DP_DISPATCH(dp, SUM_LAUNCH(PC_L132, PC_L132, DP)); break;
+        case PC_SQ64: PINS_DP_DISPATCH(dp, SUM_LAUNCH(PC_SQ64, PC_SQ64, DP)); break;
+        case PC_SQTC: PINS_DP_DISPATCH(dp, SUM_LAUNCH(PC_SQTC, PC_SQTC, DP)); break;
+        default: PINS_DP_DISPATCH(dp, SUM_LAUNCH(PC_L164, PC_L164, DP)); break;
     }
     return cudaGetLastError();
 }
@@ -598,7 +663,7 @@ int half_sweep(pins_workspace *ws, const pins_problem *pb, int o, const double *
     A.test_tol = test_tol ? 1 : 0;
     A.sink_tol = ptr<double>(ws->tol);
     const int cost = o == 0 ? ws->cost_row : ws->cost_col;
-    PINS_CUDA(launch_lse(cost, ws->dp, A.G0, st, A));
+    PINS_CUDA(launch_lse(cost, ws->dp, A.G0, st, A, o == 0 ? ws->tm_row : ws->tm_col));
     return PINS_OK;
 }
 
@@ -682,7 +747,7 @@ int run_eval(pins_workspace *ws, const pins_problem *pb, const double *phi, cons
             A.side[0].bv = ptr<double>(ws->bv);
         }
         A.a_dot = pb->a; A.f_dot = f; A.b_dot = pb->b; A.g_dot = g;
-        PINS_CUDA(launch_sum(ws->cost_row, ws->dp, A.G0 + G1, st, A));
+        PINS_CUDA(launch_sum(ws->cost_row, ws->dp, A.G0 + G1, st, A, ws->tm_row, ws->tm_col));
         PINS_CUDA(cudaMemcpyAsync(ws->h, ws->pst.p, 12 * sizeof(double), cudaMemcpyDeviceToHost, st));
         PINS_CUDA(cudaStreamSynchronize(st));
         const double *h = ws->h;

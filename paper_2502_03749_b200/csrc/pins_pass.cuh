@@ -31,6 +31,8 @@
 // order by the last CTA of each row block (atomic ticket), then per-block
 // scalars merged in block order by the last row block of the launch.
 #pragma once
+#include <cuda.h>
+
 #include "pins_device.cuh"
 #include "pins_tc.cuh"
 
@@ -52,7 +54,55 @@ enum : int {
     PC_SQ64 = 4,        // generic points, fp64: D = sum (x - y)^2
     PC_L164 = 5,        // generic points, fp64: D = sum |x - y|
     PC_SQTC = 6,        // integer points |x| <= 2048: x.y on the tensor cores (tcgen05, fp16 exact)
+    PC_DENSE_ROW_T = 7, // dense C, row orientation: 128 x 32 tiles staged by TMA (SWIZZLE_128B)
+    PC_DENSE_COL_T = 8, // dense C, column orientation: 32 x 128 tiles staged by TMA
 };
+
+// TMA staging of dense C (PC_DENSE_*_T): a ring of kNSt tiles of kTileB bytes in
+// dynamic shared memory, one mbarrier per stage (pins_api.cu builds the tensor
+// maps: row orientation boxes of {16 columns, 128 rows} with the 128-byte swizzle,
+// so thread = row reads its 32 columns without bank conflicts; column orientation
+// one box of {128 columns, 32 rows}, thread = column).
+template <int COST>
+constexpr bool kTma = COST == PC_DENSE_ROW_T || COST == PC_DENSE_COL_T;
+constexpr int kNSt = 2;                      // ring stages
+constexpr int kTileB = kCC * kPT * 8;        // 32 KB per stage
+constexpr int kTmaSmem = kNSt * kTileB + 1024;   // + alignment slack (SWIZZLE_128B: 1024 B)
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int x, int y, uint64_t *mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+        ::"r"(tc::smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(tc::smem_u32(mbar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tc::smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+}
+
+// per-CTA TMA ring state
+struct TmaRing {
+    unsigned char *base;                     // 1024-aligned ring in dynamic shared memory
+    uint64_t *full;                          // [kNSt] mbarriers (static shared memory)
+    const CUtensorMap *tm;                   // the orientation's tensor map (kernel parameter)
+    int x0;                                  // row orientation: unused; column orientation: first C column
+    int y0;                                  // row orientation: first C row; column orientation: unused
+};
+
+// thread 0: load chunk c (columns jb + c kCC of the pass) into stage c % kNSt
+template <int COST>
+__device__ __forceinline__ void tma_issue(const TmaRing &R, long long jb, long long c) {
+    const int s = (int)(c % kNSt);
+    unsigned char *dst = R.base + s * kTileB;
+    const int p = (int)(jb + c * kCC);      // first pass column of the chunk
+    mbar_expect_tx(&R.full[s], kTileB);
+    if constexpr (COST == PC_DENSE_ROW_T) {  // C rows y0.., columns p..p+31: two 16-column boxes
+        tma_load_2d(dst, R.tm, p, R.y0, &R.full[s]);
+        tma_load_2d(dst + kTileB / 2, R.tm, p + 16, R.y0, &R.full[s]);
+    } else {                                 // C rows p..p+31, columns x0..x0+127
+        tma_load_2d(dst, R.tm, R.x0, p, &R.full[s]);
+    }
+}
 
 struct PassSide {
     long long M, N;                 // pass rows / pass columns
@@ -171,7 +221,7 @@ struct Buf {
 };
 
 template <int COST>
-constexpr int kNBuf = COST == PC_DENSE_ROW ? 1 : 2;
+constexpr int kNBuf = COST == PC_DENSE_ROW ? 1 : 2;   // (the TMA ring stages dense C separately)
 
 // Whole-chunk skip by drift certificates (R10, tile form).  An entry passes the
 // per-entry fp32 test iff fl(qs_j - w_lo Df_ij) > thr32_i, i.e. (fl monotone,
@@ -375,8 +425,8 @@ struct RowPt {
 template <int COST, int DP>
 __device__ __forceinline__ double dist_global(const PassSide &P, const RowPt<COST, DP> &rp, long long i,
                                               long long j) {
-    if constexpr (COST == PC_DENSE_ROW) return P.C[i * P.ldc + j];
-    else if constexpr (COST == PC_DENSE_COL) return P.C[j * P.ldc + i];
+    if constexpr (COST == PC_DENSE_ROW || COST == PC_DENSE_ROW_T) return P.C[i * P.ldc + j];
+    else if constexpr (COST == PC_DENSE_COL || COST == PC_DENSE_COL_T) return P.C[j * P.ldc + i];
     else if constexpr (COST == PC_SQ32 || COST == PC_SQTC) {
         float dot = 0.f;
 #pragma unroll
@@ -461,7 +511,7 @@ __device__ __forceinline__ int precheck_chunks(const PassSide &P, const SkipCtx 
 template <int COST, int DP, class TS, class Body>
 __device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, long long jb, long long je,
                                               double inv_eta, int qmode, bool trial, Buf<COST, DP> *bufs,
-                                              TS *tcs, const SkipCtx &sk, Body body) {
+                                              TS *tcs, const SkipCtx &sk, const TmaRing &ring, Body body) {
     constexpr int NB = kNBuf<COST>;
     const long long nch = (je - jb + kCC - 1) / kCC;
     if (nch <= 0) return 0;
@@ -470,7 +520,7 @@ __device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, l
     constexpr uint32_t idesc = tc::make_idesc(kCC);
     auto nc_of = [&](long long c) { return (int)min((long long)kCC, je - (jb + c * kCC)); };
     __shared__ unsigned bm[kSkipWords];
-    const bool pre = NB > 1 && sk.kind == 1 && nch <= 32LL * kSkipWords;
+    const bool pre = NB > 1 && !kTma<COST> && sk.kind == 1 && nch <= 32LL * kSkipWords;
     int nskip = 0;
     if (pre) nskip = precheck_chunks(P, sk, jb, je, nch, inv_eta, qmode, trial, bm);
     // next kept chunk after c (nch: none)
@@ -488,7 +538,13 @@ __device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, l
     if (cur >= nch) return nskip;
     long long nxt = next_of(cur);
     uint32_t par = 0u;                               // bit b: parity of buffer b's next phase
-    // prologue: the first chunk into buffer 0, prefetch the next
+    // prologue: dense TMA tiles of the first kNSt - 1 chunks in flight (chunks are
+    // consecutive: no skipping on dense costs), the first chunk into buffer 0,
+    // prefetch the next
+    if constexpr (kTma<COST>) {
+        if (tid == 0)
+            for (long long c = 0; c < kNSt - 1 && c < nch; ++c) tma_issue<COST>(ring, jb, c);
+    }
     pf.load(P, jb + cur * kCC, nc_of(cur), trial, sk);
     pf.store(bufs[0], P, i0, jb + cur * kCC, nc_of(cur), inv_eta, qmode, trial, sk);
     if (trial) { __syncthreads(); pf.store_trial_qt(bufs[0], sk, jb + cur * kCC, nc_of(cur)); }
@@ -511,6 +567,9 @@ __device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, l
                 const int nb = b ^ 1;
                 if constexpr (COST == PC_SQTC) tc::fence_before();
                 __syncthreads();                         // the previous chunk fully consumed
+                if constexpr (kTma<COST>) {              // its stage is free: refill kNSt - 1 ahead
+                    if (tid == 0 && cur + kNSt - 1 < nch) tma_issue<COST>(ring, jb, cur + kNSt - 1);
+                }
                 pf.store(bufs[nb], P, i0, jb + nxt * kCC, nc_of(nxt), inv_eta, qmode, trial, sk);
                 if (trial) { __syncthreads(); pf.store_trial_qt(bufs[nb], sk, jb + nxt * kCC, nc_of(nxt)); }
                 nxt2 = next_of(nxt);
@@ -542,7 +601,12 @@ __device__ __forceinline__ int stream_columns(const PassSide &P, long long i0, l
             tc::fence_after();
             tc::ld32(tcs->tbase + ((uint32_t)(32 * (warp & 3)) << 16) + b * kCC, dots);
         }
-        body(jb + cur * kCC, nc_of(cur), bufs[b], dots);
+        const unsigned char *tile = nullptr;
+        if constexpr (kTma<COST>) {                   // this chunk's C tile has landed
+            tc::mbar_wait(&ring.full[cur % kNSt], (uint32_t)((cur / kNSt) & 1));
+            tile = ring.base + (cur % kNSt) * kTileB;
+        }
+        body(jb + cur * kCC, nc_of(cur), bufs[b], dots, tile);
         cur = nxt;
         nxt = nxt2;
         if (NB > 1) b ^= 1;
@@ -622,11 +686,33 @@ __device__ __forceinline__ void tc_teardown(TS &T) {
     }
 }
 
+// CTA-level TMA ring setup (dense costs staged by TMA): 1024-aligned ring in
+// dynamic shared memory, one mbarrier per stage (contains __syncthreads)
+template <int COST>
+__device__ __forceinline__ TmaRing ring_setup(unsigned char *dyn, uint64_t *full, const CUtensorMap *tm, long long i0) {
+    TmaRing R{nullptr, full, tm, (int)i0, (int)i0};
+    if constexpr (kTma<COST>) {
+        R.base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(dyn) + 1023) & ~uintptr_t(1023));
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < kNSt; ++s) tc::mbar_init(&full[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+    }
+    return R;
+}
+
 // D(i, j0 + c) for the non-tensor-core costs from the staged chunk
 template <int COST, int DP>
 __device__ __forceinline__ double chunk_dist(const Buf<COST, DP> &B, const PassSide &P, const RowPt<COST, DP> &rp,
-                                             long long i, long long j0, int c) {
-    if constexpr (COST == PC_DENSE_ROW) return B.tile[c * (kPT + 1) + threadIdx.x];
+                                             long long i, long long j0, int c, const unsigned char *tile) {
+    if constexpr (COST == PC_DENSE_ROW_T) {       // swizzled {16 x 128} box c / 16, row = thread
+        const int t = threadIdx.x, cc = c & 15;
+        return *reinterpret_cast<const double *>(tile + (c >> 4) * (kTileB / 2) + t * 128 +
+                                                 ((((cc >> 1) ^ (t & 7))) << 4) + (cc & 1) * 8);
+    } else if constexpr (COST == PC_DENSE_COL_T) { // {128 x 32} box, column = thread
+        return *reinterpret_cast<const double *>(tile + c * (kPT * 8) + threadIdx.x * 8);
+    } else if constexpr (COST == PC_DENSE_ROW) return B.tile[c * (kPT + 1) + threadIdx.x];
     else if constexpr (COST == PC_DENSE_COL) return __ldg(P.C + (j0 + c) * P.ldc + i);
     else if constexpr (COST == PC_SQTC) return 0.0;
     else return rp.dist(B, c);
@@ -707,7 +793,8 @@ __device__ __forceinline__ void record_cert(const SkipCtx &sk, long long j0, flo
 template <int COST, int DP>
 __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSide &P, const RowPt<COST, DP> &rp,
                                            long long i, long long j0, int nc, const float *dots, float w_lo,
-                                           float thr32, float (&Dv)[COST == PC_SQTC ? kCC : 1], float &vmx) {
+                                           float thr32, float (&Dv)[COST == PC_SQTC ? kCC : 1], float &vmx,
+                                           const unsigned char *tile) {
     unsigned mask = 0u;
 #pragma unroll
     for (int c4 = 0; c4 < kCC; c4 += 4) {
@@ -726,7 +813,7 @@ __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSid
                 Df = fmaf(-2.f, dots[c], rp.nx + nyv[j]);
                 Dv[c] = Df;
             } else {
-                Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+                Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c, tile);
             }
             const float v = fmaf(-w_lo, Df, qsv[j]);
             vmx = c < nc ? fmaxf(vmx, v) : vmx;
@@ -742,7 +829,9 @@ __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSid
 // the starting iterate (pass-row side), st[1] = max |f_new - f_old|.
 // =========================================================================
 template <int COST, int DP>
-__global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A) {
+__global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __grid_constant__ CUtensorMap tm0) {
+    extern __shared__ __align__(1024) unsigned char dyn_smem[];   // TMA ring (dense costs) or unused
+    __shared__ uint64_t ring_full[kNSt];
     __shared__ Buf<COST, DP> bufs[kNBuf<COST>];
     __shared__ TcFor<COST> tcs_storage[1];
     __shared__ float dscr[COST == PC_SQTC ? kPT * (kCC + 1) : 1];
@@ -776,15 +865,17 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A) {
     int nsurv = 0;
     const float thr0 = thr_lo_of(mx - kLseCut);
     const SkipCtx sk = skip_setup(P, rb, sp, i, valid, jb, thr0, w_lo, red);
-    const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, 0, false, bufs, &tcs, sk,
-                             [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
+    const TmaRing ring = ring_setup<COST>(dyn_smem, ring_full, &tm0, i0);
+    const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, 0, false, bufs, &tcs, sk, ring,
+                             [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots,
+                                 const unsigned char *tile) {
         // phase 1: skip test against the chunk-start bound of the row max
         const float thr32 = thr_lo_of(mx - kLseCut);
         unsigned mask = 0u;
         float vmx = -INFINITY;
         float Dv[COST == PC_SQTC ? kCC : 1];
         if (valid)
-            mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx);
+            mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, tile);
         if (sk.kind == 2) record_cert(sk, j0, vmx, thr0, valid);
         nsurv += __popc(mask);
         if (!valid) return;
@@ -801,7 +892,7 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A) {
             mask &= mask - 1u;
             double D;
             if constexpr (COST == PC_SQTC) D = (double)dsc[c];
-            else D = chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+            else D = chunk_dist<COST, DP>(B, P, rp, i, j0, c, tile);
             const double x = fma(-w, D, B.q[c]);
             const double d = x - mx;
             const double e = pexp_lean(fmax(-745.0, -fabs(d)), thi, tlo);
@@ -884,7 +975,8 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A) {
 template <int COST, int DP, class TS>
 __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, int bid, Buf<COST, DP> *bufs,
                                          TS &tcs, float *dscr, double *thi, double *tlo, double *red,
-                                         bool *flag, int side) {
+                                         bool *flag, int side, unsigned char *dyn, uint64_t *ring_full,
+                                         const CUtensorMap *tm) {
     const int tid = threadIdx.x;
     const int rb = bid % P.RB, sp = bid / P.RB;
     const long long i0 = (long long)rb * kPT, i = i0 + tid;
@@ -912,13 +1004,15 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
     float *dsc = dscr + tid * (kCC + 1);
     int nsurv = 0;
     const SkipCtx sk = skip_setup(P, rb, sp, i, valid, jb, thr32, w_lo, red);
-    const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, P.m1_row ? 0 : 1, trial, bufs, &tcs, sk,
-                             [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots) {
+    const TmaRing ring = ring_setup<COST>(dyn, ring_full, tm, i0);
+    const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, P.m1_row ? 0 : 1, trial, bufs, &tcs, sk, ring,
+                             [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots,
+                                 const unsigned char *tile) {
         unsigned mask = 0u;
         float vmx = -INFINITY;
         float Dv[COST == PC_SQTC ? kCC : 1];
         if (valid)
-            mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx);
+            mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, tile);
         if (sk.kind == 2) record_cert(sk, j0, vmx, thr32, valid);
         nsurv += __popc(mask);
         if (!valid) return;
@@ -934,7 +1028,7 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
             mask &= mask - 1u;
             double D;
             if constexpr (COST == PC_SQTC) D = (double)dsc[c];
-            else D = chunk_dist<COST, DP>(B, P, rp, i, j0, c);
+            else D = chunk_dist<COST, DP>(B, P, rp, i, j0, c, tile);
             const double z = fma(-w, D, __dadd_rn(Pi, B.q[c]));
             const double X = pexp_lean(fmin(709.0, fmax(-745.0, z)), thi, tlo);
             acc += X;
@@ -1015,7 +1109,10 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
 }
 
 template <int COST0, int COST1, int DP>
-__global__ void __launch_bounds__(kPT) sum_pass_kernel(PassArgs A) {
+__global__ void __launch_bounds__(kPT) sum_pass_kernel(PassArgs A, const __grid_constant__ CUtensorMap tm0,
+                                                       const __grid_constant__ CUtensorMap tm1) {
+    extern __shared__ __align__(1024) unsigned char dyn_smem[];   // TMA ring (dense costs) or unused
+    __shared__ uint64_t ring_full[kNSt];
     constexpr size_t kB0 = sizeof(Buf<COST0, DP>) * kNBuf<COST0>, kB1 = sizeof(Buf<COST1, DP>) * kNBuf<COST1>;
     __shared__ __align__(128) unsigned char smraw[kB0 > kB1 ? kB0 : kB1];
     __shared__ TcFor<(COST0 == PC_SQTC || COST1 == PC_SQTC) ? PC_SQTC : COST0> tcs;
@@ -1027,9 +1124,11 @@ __global__ void __launch_bounds__(kPT) sum_pass_kernel(PassArgs A) {
     const int side = (blockIdx.x < (unsigned)A.G0) ? 0 : 1;
     const int bid = side == 0 ? blockIdx.x : blockIdx.x - A.G0;
     if (side == 0)
-        sum_side<COST0, DP>(A, A.side[0], bid, reinterpret_cast<Buf<COST0, DP> *>(smraw), tcs, dscr, thi, tlo, red, &flag, 0);
+        sum_side<COST0, DP>(A, A.side[0], bid, reinterpret_cast<Buf<COST0, DP> *>(smraw), tcs, dscr, thi, tlo, red,
+                            &flag, 0, dyn_smem, ring_full, &tm0);
     else
-        sum_side<COST1, DP>(A, A.side[1], bid, reinterpret_cast<Buf<COST1, DP> *>(smraw), tcs, dscr, thi, tlo, red, &flag, 1);
+        sum_side<COST1, DP>(A, A.side[1], bid, reinterpret_cast<Buf<COST1, DP> *>(smraw), tcs, dscr, thi, tlo, red,
+                            &flag, 1, dyn_smem, ring_full, &tm1);
     // only row-block finalizers continue past here with flag set
     if (!flag) return;
     const unsigned tot = (unsigned)(A.side[0].RB + (A.nsides > 1 ? A.side[1].RB : 0));

@@ -70,7 +70,9 @@ CASES = [
     ("c2s", lambda: make("c2_img4k", scale=0.06)),
     ("c3s", lambda: make("c3_gmm10k", scale=0.013)),
     ("c4s", lambda: make("c4_l1rect", scale=0.012)),
-    ("rag_dense", lambda: ragged(37, 1029, 5)),
+    ("rag_dense", lambda: ragged(37, 1029, 5)),           # odd pitch: thread-staged dense path
+    ("c1t", lambda: make("c1_rand1k", scale=0.125)),      # 128 x 128: TMA-staged dense path
+    ("rag_dense_t", lambda: ragged(37, 1030, 15)),        # even pitch, ragged: TMA path, partial tiles
     ("rag_sq", lambda: ragged(70, 515, 6, "sq", 10)),
     ("rag_l1", lambda: ragged(33, 17, 7, "l1", 3)),
     # real-valued point sets (BASELINE.json as written): fp64 cost paths PC_SQ64 / PC_L164
@@ -504,6 +506,37 @@ def test_tensor_core_cross_term_bit_identical(P, name, mk, monkeypatch):
         fd, gd = T(f), T(g)
         for _ in range(2):
             P.sinkhorn_sweep(ws, pb, T(phi), T(psi), s, fd, gd)
+        out.append((H(ev["r"]), H(ev["c"]), ev["cost"], ev["grad_l1"], csr, H(fd), H(gd)))
+    a, b = out
+    for x, y in zip(a[:2], b[:2]):
+        assert np.array_equal(x, y)
+    assert a[2] == b[2] and a[3] == b[3]
+    for x, y in zip(a[4], b[4]):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a[5], b[5]) and np.array_equal(a[6], b[6])
+
+
+@pytest.mark.parametrize("name,mk", [("c1t", lambda: make("c1_rand1k", scale=0.3)),
+                                     ("rag_dense_t", lambda: ragged(301, 1030, 19)),
+                                     ("tall", lambda: ragged(1030, 66, 20))])
+def test_tma_staged_dense_passes_bit_identical(P, name, mk, monkeypatch):
+    # dense C tiles staged by TMA (cp.async.bulk.tensor, 128-byte swizzle for the row
+    # orientation) feed the same arithmetic in the same order as the thread-staged path:
+    # every pass must agree bit for bit (PINS_NO_TMA=1 selects the thread-staged path)
+    w = mk()
+    assert w.n % 2 == 0
+    C, Ck, phi, psi, s, f, g = oracle_state(w, 1)
+    tau = 1e-4 / (w.m * w.n)
+    out = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("PINS_NO_TMA", "1")
+        pb = P.DeviceProblem.from_workload(w)
+        ws = P.Workspace()
+        ev = P.evaluate(ws, pb, T(phi), T(psi), s, T(f), T(g), tau=tau)
+        csr = [H(t_) for t_ in P.get_csr(ws)]
+        fd, gd = T(f), T(g)
+        P.sinkhorn(ws, pb, T(phi), T(psi), s, fd, gd, 0.0, 7)
         out.append((H(ev["r"]), H(ev["c"]), ev["cost"], ev["grad_l1"], csr, H(fd), H(gd)))
     a, b = out
     for x, y in zip(a[:2], b[:2]):
