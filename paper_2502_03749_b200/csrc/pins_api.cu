@@ -591,20 +591,21 @@ void fill_side(pins_workspace *ws, const pins_problem *pb, int o, const double *
 // dynamic shared memory of a pass kernel instantiation: the TMA ring for dense
 // costs staged by TMA (attribute set once per instantiation), else none
 template <class K>
-size_t pass_smem(K kern, bool tma) {
-    if (!tma) return 0;
+size_t pass_smem(K kern, size_t bytes) {
+    if (!bytes) return 0;
     static bool done = false;
     if (!done) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         done = true;
     }
-    return kTmaSmem;
+    return bytes;
 }
 #define LSE_LAUNCH(CLS, C_, DP_)                                                                            \
-    LAUNCH(CLS, st, lse_pass_kernel<C_, DP_><<<grid, kPT, pass_smem(lse_pass_kernel<C_, DP_>, kTma<C_>), st>>>(A, tm))
+    LAUNCH(CLS, st, lse_pass_kernel<C_, DP_><<<grid, kPT,                                                     \
+           pass_smem(lse_pass_kernel<C_, DP_>, (kTma<C_> ? kTmaSmem : 0) + (kWC<C_> ? kWCSmem : 0)), st>>>(A, tm))
 #define SUM_LAUNCH(C0_, C1_, DP_)                                                                            \
     LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<C0_, C1_, DP_><<<grid, kPT,                                    \
-           pass_smem(sum_pass_kernel<C0_, C1_, DP_>, kTma<C0_>), st>>>(A, tm0, tm1))
+           pass_smem(sum_pass_kernel<C0_, C1_, DP_>, kTma<C0_> ? kTmaSmem : 0), st>>>(A, tm0, tm1))
 
 cudaError_t launch_lse(int cost, int dp, int grid, cudaStream_t st, const PassArgs &A, const CUtensorMap &tm) {
     switch (cost) {

@@ -65,6 +65,11 @@ enum : int {
 // one box of {128 columns, 32 rows}, thread = column).
 template <int COST>
 constexpr bool kTma = COST == PC_DENSE_ROW_T || COST == PC_DENSE_COL_T;
+// half-sweeps with the warp-cooperative phase 2 (distances reachable by any lane)
+template <int COST>
+constexpr bool kWC = COST == PC_SQTC || COST == PC_SQ32 || COST == PC_L132 || COST == PC_DENSE_ROW ||
+                     COST == PC_DENSE_COL || COST == PC_DENSE_ROW_T || COST == PC_DENSE_COL_T;
+constexpr int kWCSmem = 128 * 32 * 8 + 128 * 32 * 2 + 128 * 8 + 16;   // partials, queue, references
 constexpr int kNSt = 2;                      // ring stages
 constexpr int kTileB = kCC * kPT * 8;        // 32 KB per stage
 constexpr int kTmaSmem = kNSt * kTileB + 1024;   // + alignment slack (SWIZZLE_128B: 1024 B)
@@ -718,6 +723,26 @@ __device__ __forceinline__ double chunk_dist(const Buf<COST, DP> &B, const PassS
     else return rp.dist(B, c);
 }
 
+// D(pass row t of the CTA (global i), j0 + c) from the staged chunk, for any
+// thread of the CTA (warp-cooperative phase 2 of the half-sweep)
+template <int COST, int DP>
+__device__ __forceinline__ double chunk_dist_of(const Buf<COST, DP> &B, const PassSide &P, const float *dscr,
+                                                int t, long long i, long long j0, int c, const unsigned char *tile) {
+    if constexpr (COST == PC_DENSE_ROW_T) {
+        const int cc = c & 15;
+        return *reinterpret_cast<const double *>(tile + (c >> 4) * (kTileB / 2) + t * 128 +
+                                                 ((((cc >> 1) ^ (t & 7))) << 4) + (cc & 1) * 8);
+    } else if constexpr (COST == PC_DENSE_COL_T) {
+        return *reinterpret_cast<const double *>(tile + c * (kPT * 8) + t * 8);
+    } else if constexpr (COST == PC_DENSE_ROW) {
+        return B.tile[c * (kPT + 1) + t];
+    } else if constexpr (COST == PC_DENSE_COL) {
+        return __ldg(P.C + (j0 + c) * P.ldc + i);
+    } else {                                        // exact fp32 distances stored by phase 1
+        return (double)dscr[t * (kCC + 1) + c];
+    }
+}
+
 // ----------------------------------------------------- ticket helpers
 // returns true in exactly one CTA: the last of `total` arrivals on *t (then reset)
 __device__ __forceinline__ bool last_arrival(unsigned *t, unsigned total, bool *sh_flag) {
@@ -790,10 +815,14 @@ __device__ __forceinline__ void record_cert(const SkipCtx &sk, long long j0, flo
 // phase 1 of a chunk (branch-free): the survivor mask of the fp32 test
 // fl(qs_j - w_lo D_ij) > thr32, the fp32 distances (PC_SQTC) and the row's
 // maximum test value (used by reference passes)
+// costs whose exact fp32 distances phase 1 keeps (for phase 2 through shared memory)
+template <int COST>
+constexpr bool kDv = COST == PC_SQTC || COST == PC_SQ32 || COST == PC_L132;
+
 template <int COST, int DP>
 __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSide &P, const RowPt<COST, DP> &rp,
                                            long long i, long long j0, int nc, const float *dots, float w_lo,
-                                           float thr32, float (&Dv)[COST == PC_SQTC ? kCC : 1], float &vmx,
+                                           float thr32, float (&Dv)[kDv<COST> ? kCC : 1], float &vmx,
                                            const unsigned char *tile) {
     unsigned mask = 0u;
 #pragma unroll
@@ -814,6 +843,7 @@ __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSid
                 Dv[c] = Df;
             } else {
                 Df = (float)chunk_dist<COST, DP>(B, P, rp, i, j0, c, tile);
+                if constexpr (kDv<COST>) Dv[c] = Df;
             }
             const float v = fmaf(-w_lo, Df, qsv[j]);
             vmx = c < nc ? fmaxf(vmx, v) : vmx;
@@ -834,7 +864,7 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
     __shared__ uint64_t ring_full[kNSt];
     __shared__ Buf<COST, DP> bufs[kNBuf<COST>];
     __shared__ TcFor<COST> tcs_storage[1];
-    __shared__ float dscr[COST == PC_SQTC ? kPT * (kCC + 1) : 1];
+    __shared__ float dscr[kDv<COST> ? kPT * (kCC + 1) : 1];
     __shared__ double thi[64], tlo[64];
     __shared__ double red[kPT / 32];
     __shared__ bool flag;
@@ -852,16 +882,32 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
     rp.load(P, i, valid);
     const double w = A.w, inv_eta = A.inv_eta;
     const float w_lo = (float)w * (1.f - 0x1p-19f);
-    double mx = -INFINITY, sm = 0.0;
+    double mx = -INFINITY, sm = 0.0;       // the row's reference (a true entry) and sum exp(x - mx)
     int jm = -1;
     if (valid) {
         const int js = P.jstar[i];
         if (js >= 0 && js < P.N) {     // lower bound of the row max: one true entry
             const double D = dist_global<COST, DP>(P, rp, i, js);
             mx = fma(-w, D, pot_q(P.gc[js], P.psic[js], inv_eta));
+            jm = js;
         }
     }
-    float *dsc = dscr + tid * (kCC + 1);       // PC_SQTC: this thread's chunk distances
+    const int lane = tid & 31, warp = tid >> 5;
+    // warp-cooperative phase 2 (kWC): per-(row, lane) partial sums, the survivor queue
+    // and the rows' references live in dynamic shared memory after the TMA ring
+    double *part = nullptr;                    // [4 warps][32 rows][32 lanes]
+    unsigned short *queue = nullptr;           // [4 warps][1024]
+    double *Mrow = nullptr;                    // [128]
+    if constexpr (kWC<COST>) {
+        unsigned char *wc = dyn_smem + (kTma<COST> ? kTmaSmem : 0);
+        wc = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(wc) + 15) & ~uintptr_t(15));
+        part = reinterpret_cast<double *>(wc);
+        queue = reinterpret_cast<unsigned short *>(wc + kPT * 32 * 8);
+        Mrow = reinterpret_cast<double *>(wc + kPT * 32 * 8 + kPT * 32 * 2);
+        for (int r = 0; r < 32; ++r) part[(tid * 32) + r] = 0.0;
+        Mrow[tid] = mx;
+    }
+    float *dsc = dscr + tid * (kCC + 1);       // this thread's chunk distances (kDv costs)
     int nsurv = 0;
     const float thr0 = thr_lo_of(mx - kLseCut);
     const SkipCtx sk = skip_setup(P, rb, sp, i, valid, jb, thr0, w_lo, red);
@@ -873,35 +919,95 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
         const float thr32 = thr_lo_of(mx - kLseCut);
         unsigned mask = 0u;
         float vmx = -INFINITY;
-        float Dv[COST == PC_SQTC ? kCC : 1];
+        float Dv[kDv<COST> ? kCC : 1];
         if (valid)
             mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, tile);
         if (sk.kind == 2) record_cert(sk, j0, vmx, thr0, valid);
         nsurv += __popc(mask);
-        if (!valid) return;
-        if constexpr (COST == PC_SQTC) {
+        if constexpr (kDv<COST>) {
             // distances are needed only where some lane of the warp has a survivor
-            if (__any_sync(__activemask(), mask != 0u)) {
+            if (__any_sync(0xffffffffu, mask != 0u)) {
 #pragma unroll
                 for (int c = 0; c < kCC; ++c) dsc[c] = Dv[c];
             }
         }
-        // phase 2: the surviving entries of this row, in column order (one exp each)
-        while (mask) {
-            const int c = __ffs(mask) - 1;
-            mask &= mask - 1u;
-            double D;
-            if constexpr (COST == PC_SQTC) D = (double)dsc[c];
-            else D = chunk_dist<COST, DP>(B, P, rp, i, j0, c, tile);
-            const double x = fma(-w, D, B.q[c]);
-            const double d = x - mx;
-            const double e = pexp_lean(fmax(-745.0, -fabs(d)), thi, tlo);
-            const bool up = d > 0.0;
-            sm = up ? fma(sm, e, 1.0) : sm + e;
-            mx = up ? x : mx;
-            jm = up ? (int)(j0 + c) : jm;
+        if constexpr (kWC<COST>) {
+            // (a) reference update (rare): when an entry may exceed the reference by more
+            // than one e-fold, the row's reference becomes the exact maximum over its
+            // survivors (a true entry) and its partial sums are rescaled
+            if (mask != 0u && (mx == -INFINITY || vmx > (float)(mx + 1.0))) {
+                double xm = -INFINITY;
+                int cm = -1;
+                for (unsigned mm = mask; mm; mm &= mm - 1u) {
+                    const int c = __ffs(mm) - 1;
+                    const double x = fma(-w, chunk_dist_of<COST, DP>(B, P, dscr, tid, i, j0, c, tile), B.q[c]);
+                    if (x > xm) { xm = x; cm = c; }
+                }
+                if (xm > mx) {
+                    if (mx != -INFINITY) {
+                        const double sc = pexp_lean(fmax(-745.0, mx - xm), thi, tlo);
+                        for (int r = 0; r < 32; ++r) {       // rotated: conflict-free
+                            const int q = (r + lane) & 31;
+                            part[tid * 32 + q] *= sc;
+                        }
+                    }
+                    mx = xm;
+                    jm = (int)(j0 + cm);
+                    Mrow[tid] = mx;
+                }
+            }
+            __syncwarp();
+            // (b) survivor queue of the warp: entry = (row lane << 5) | column, row-major
+            const int cnt = __popc(mask);
+            int pre = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, pre, o);
+                if (lane >= o) pre += t;
+            }
+            const int tot = __shfl_sync(0xffffffffu, pre, 31);
+            pre -= cnt;
+            unsigned short *qw = queue + warp * 1024;
+            for (unsigned mm = mask; mm; mm &= mm - 1u) qw[pre++] = (unsigned short)((lane << 5) | (__ffs(mm) - 1));
+            __syncwarp();
+            // (c) 32 survivors per round, one per lane: exp(x - reference of its row),
+            // added to the (row, lane) partial sum -- all lanes busy, no atomics
+            for (int base = 0; base < tot; base += 32) {
+                const int k = base + lane;
+                if (k < tot) {
+                    const int e16 = qw[k];
+                    const int rl = e16 >> 5, c = e16 & 31;
+                    const int t = warp * 32 + rl;
+                    const double D = chunk_dist_of<COST, DP>(B, P, dscr, t, i0 + t, j0, c, tile);
+                    const double x = fma(-w, D, B.q[c]);
+                    const double e = pexp_lean(fmin(709.0, fmax(-745.0, x - Mrow[t])), thi, tlo);
+                    part[t * 32 + lane] += e;
+                }
+            }
+            __syncwarp();
+        } else {
+            if (!valid) return;
+            // phase 2: the surviving entries of this row, in column order (one exp each)
+            while (mask) {
+                const int c = __ffs(mask) - 1;
+                mask &= mask - 1u;
+                const double D = chunk_dist<COST, DP>(B, P, rp, i, j0, c, tile);
+                const double x = fma(-w, D, B.q[c]);
+                const double d = x - mx;
+                const double e = pexp_lean(fmax(-745.0, -fabs(d)), thi, tlo);
+                const bool up = d > 0.0;
+                sm = up ? fma(sm, e, 1.0) : sm + e;
+                mx = up ? x : mx;
+                jm = up ? (int)(j0 + c) : jm;
+            }
         }
     });
+    if constexpr (kWC<COST>) {
+        __syncwarp();
+        double t = 0.0;
+        for (int r = 0; r < 32; ++r) t += part[tid * 32 + ((r + lane) & 31)];
+        sm = t;
+    }
     if constexpr (COST == PC_SQTC) tc_teardown(tcs);
     skip_count(P, sk, nskip, jb, je);
     count_survivors(A.count_surv, 0, nsurv);
@@ -1010,7 +1116,7 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
                                  const unsigned char *tile) {
         unsigned mask = 0u;
         float vmx = -INFINITY;
-        float Dv[COST == PC_SQTC ? kCC : 1];
+        float Dv[kDv<COST> ? kCC : 1];
         if (valid)
             mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, tile);
         if (sk.kind == 2) record_cert(sk, j0, vmx, thr32, valid);
