@@ -602,7 +602,7 @@ size_t pass_smem(K kern, size_t bytes) {
 }
 #define LSE_LAUNCH(CLS, C_, DP_)                                                                            \
     LAUNCH(CLS, st, lse_pass_kernel<C_, DP_><<<grid, kPT,                                                     \
-           pass_smem(lse_pass_kernel<C_, DP_>, (kTma<C_> ? kTmaSmem : 0) + (kWC<C_> ? kWCSmem : 0)), st>>>(A, tm))
+           pass_smem(lse_pass_kernel<C_, DP_>, kTma<C_> ? kTmaSmem : 0), st>>>(A, tm))
 #define SUM_LAUNCH(C0_, C1_, DP_)                                                                            \
     LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<C0_, C1_, DP_><<<grid, kPT,                                    \
            pass_smem(sum_pass_kernel<C0_, C1_, DP_>, kTma<C0_> ? kTmaSmem : 0), st>>>(A, tm0, tm1))

@@ -65,11 +65,6 @@ enum : int {
 // one box of {128 columns, 32 rows}, thread = column).
 template <int COST>
 constexpr bool kTma = COST == PC_DENSE_ROW_T || COST == PC_DENSE_COL_T;
-// half-sweeps with the warp-cooperative phase 2 (distances reachable by any lane)
-template <int COST>
-constexpr bool kWC = COST == PC_SQTC || COST == PC_SQ32 || COST == PC_L132 || COST == PC_DENSE_ROW ||
-                     COST == PC_DENSE_COL || COST == PC_DENSE_ROW_T || COST == PC_DENSE_COL_T;
-constexpr int kWCSmem = 128 * 32 * 8 + 128 * 32 * 2 + 128 * 8 + 16;   // partials, queue, references
 constexpr int kNSt = 2;                      // ring stages
 constexpr int kTileB = kCC * kPT * 8;        // 32 KB per stage
 constexpr int kTmaSmem = kNSt * kTileB + 1024;   // + alignment slack (SWIZZLE_128B: 1024 B)
@@ -175,6 +170,15 @@ struct PassArgs {
     int test_tol;                   // LSE row pass: set done (and rollback) when res <= tol
     const double *a_dot, *f_dot, *b_dot, *g_dot;   // SUM: <a,f> + <b,g> (global finalize)
 };
+
+// Column range of split sp of S: whole kCC-column chunks (so every chunk starts at
+// a multiple of kCC -- TMA box origins stay 256-byte aligned), the last split
+// ending at N.
+__device__ __forceinline__ void split_range(long long N, int S, int sp, long long &jb, long long &je) {
+    const long long nch = (N + kCC - 1) / kCC;
+    jb = kCC * (nch * sp / S);
+    je = min(N, kCC * (nch * (sp + 1) / S));
+}
 
 // Profiling counters (pins_prof_read_work): entries evaluated in phase 2 (the
 // survivors of the skip test), [0] half-sweeps, [1] sum passes.
@@ -723,26 +727,6 @@ __device__ __forceinline__ double chunk_dist(const Buf<COST, DP> &B, const PassS
     else return rp.dist(B, c);
 }
 
-// D(pass row t of the CTA (global i), j0 + c) from the staged chunk, for any
-// thread of the CTA (warp-cooperative phase 2 of the half-sweep)
-template <int COST, int DP>
-__device__ __forceinline__ double chunk_dist_of(const Buf<COST, DP> &B, const PassSide &P, const float *dscr,
-                                                int t, long long i, long long j0, int c, const unsigned char *tile) {
-    if constexpr (COST == PC_DENSE_ROW_T) {
-        const int cc = c & 15;
-        return *reinterpret_cast<const double *>(tile + (c >> 4) * (kTileB / 2) + t * 128 +
-                                                 ((((cc >> 1) ^ (t & 7))) << 4) + (cc & 1) * 8);
-    } else if constexpr (COST == PC_DENSE_COL_T) {
-        return *reinterpret_cast<const double *>(tile + c * (kPT * 8) + t * 8);
-    } else if constexpr (COST == PC_DENSE_ROW) {
-        return B.tile[c * (kPT + 1) + t];
-    } else if constexpr (COST == PC_DENSE_COL) {
-        return __ldg(P.C + (j0 + c) * P.ldc + i);
-    } else {                                        // exact fp32 distances stored by phase 1
-        return (double)dscr[t * (kCC + 1) + c];
-    }
-}
-
 // ----------------------------------------------------- ticket helpers
 // returns true in exactly one CTA: the last of `total` arrivals on *t (then reset)
 __device__ __forceinline__ bool last_arrival(unsigned *t, unsigned total, bool *sh_flag) {
@@ -874,7 +858,8 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
     const int rb = blockIdx.x % P.RB, sp = blockIdx.x / P.RB;
     const long long i0 = (long long)rb * kPT, i = i0 + tid;
     const bool valid = i < P.M;
-    const long long jb = P.N * sp / P.S, je = P.N * (sp + 1) / P.S;
+    long long jb, je;
+    split_range(P.N, P.S, sp, jb, je);
     load_exp_table(A.tab, thi, tlo);
     TcFor<COST> &tcs = tcs_storage[0];
     if constexpr (COST == PC_SQTC) tc_setup(tcs, P, i0);
@@ -891,21 +876,6 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
             mx = fma(-w, D, pot_q(P.gc[js], P.psic[js], inv_eta));
             jm = js;
         }
-    }
-    const int lane = tid & 31, warp = tid >> 5;
-    // warp-cooperative phase 2 (kWC): per-(row, lane) partial sums, the survivor queue
-    // and the rows' references live in dynamic shared memory after the TMA ring
-    double *part = nullptr;                    // [4 warps][32 rows][32 lanes]
-    unsigned short *queue = nullptr;           // [4 warps][1024]
-    double *Mrow = nullptr;                    // [128]
-    if constexpr (kWC<COST>) {
-        unsigned char *wc = dyn_smem + (kTma<COST> ? kTmaSmem : 0);
-        wc = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(wc) + 15) & ~uintptr_t(15));
-        part = reinterpret_cast<double *>(wc);
-        queue = reinterpret_cast<unsigned short *>(wc + kPT * 32 * 8);
-        Mrow = reinterpret_cast<double *>(wc + kPT * 32 * 8 + kPT * 32 * 2);
-        for (int r = 0; r < 32; ++r) part[(tid * 32) + r] = 0.0;
-        Mrow[tid] = mx;
     }
     float *dsc = dscr + tid * (kCC + 1);       // this thread's chunk distances (kDv costs)
     int nsurv = 0;
@@ -931,83 +901,33 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
                 for (int c = 0; c < kCC; ++c) dsc[c] = Dv[c];
             }
         }
-        if constexpr (kWC<COST>) {
-            // (a) reference update (rare): when an entry may exceed the reference by more
-            // than one e-fold, the row's reference becomes the exact maximum over its
-            // survivors (a true entry) and its partial sums are rescaled
-            if (mask != 0u && (mx == -INFINITY || vmx > (float)(mx + 1.0))) {
-                double xm = -INFINITY;
-                int cm = -1;
-                for (unsigned mm = mask; mm; mm &= mm - 1u) {
-                    const int c = __ffs(mm) - 1;
-                    const double x = fma(-w, chunk_dist_of<COST, DP>(B, P, dscr, tid, i, j0, c, tile), B.q[c]);
-                    if (x > xm) { xm = x; cm = c; }
-                }
-                if (xm > mx) {
-                    if (mx != -INFINITY) {
-                        const double sc = pexp_lean(fmax(-745.0, mx - xm), thi, tlo);
-                        for (int r = 0; r < 32; ++r) {       // rotated: conflict-free
-                            const int q = (r + lane) & 31;
-                            part[tid * 32 + q] *= sc;
-                        }
-                    }
-                    mx = xm;
-                    jm = (int)(j0 + cm);
-                    Mrow[tid] = mx;
-                }
+        if (!valid) return;
+        // phase 2: the surviving entries of this row, two per iteration (independent
+        // exponentials).  The reference mx is a true entry; sm accumulates exp(x - mx)
+        // for x <= mx + 1 and a larger x (rare once the argmax seed is in place) becomes
+        // the new reference with sm rescaled -- no per-entry max bookkeeping.
+        while (mask) {
+            const int c1 = __ffs(mask) - 1;
+            mask &= mask - 1u;
+            const bool two = mask != 0u;
+            const int c2 = two ? __ffs(mask) - 1 : c1;
+            mask &= two ? mask - 1u : mask;
+            const double D1 = kDv<COST> ? (double)dsc[c1] : chunk_dist<COST, DP>(B, P, rp, i, j0, c1, tile);
+            const double D2 = kDv<COST> ? (double)dsc[c2] : chunk_dist<COST, DP>(B, P, rp, i, j0, c2, tile);
+            const double x1 = fma(-w, D1, B.q[c1]);
+            const double x2 = fma(-w, D2, B.q[c2]);
+            if (fmax(x1, x2) > mx + 1.0) {        // new reference: the larger entry
+                const bool first = x1 >= x2;
+                const double xn = first ? x1 : x2;
+                sm = sm * pexp_lean(fmax(-745.0, mx - xn), thi, tlo);
+                mx = xn;
+                jm = (int)(j0 + (first ? c1 : c2));
             }
-            __syncwarp();
-            // (b) survivor queue of the warp: entry = (row lane << 5) | column, row-major
-            const int cnt = __popc(mask);
-            int pre = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, pre, o);
-                if (lane >= o) pre += t;
-            }
-            const int tot = __shfl_sync(0xffffffffu, pre, 31);
-            pre -= cnt;
-            unsigned short *qw = queue + warp * 1024;
-            for (unsigned mm = mask; mm; mm &= mm - 1u) qw[pre++] = (unsigned short)((lane << 5) | (__ffs(mm) - 1));
-            __syncwarp();
-            // (c) 32 survivors per round, one per lane: exp(x - reference of its row),
-            // added to the (row, lane) partial sum -- all lanes busy, no atomics
-            for (int base = 0; base < tot; base += 32) {
-                const int k = base + lane;
-                if (k < tot) {
-                    const int e16 = qw[k];
-                    const int rl = e16 >> 5, c = e16 & 31;
-                    const int t = warp * 32 + rl;
-                    const double D = chunk_dist_of<COST, DP>(B, P, dscr, t, i0 + t, j0, c, tile);
-                    const double x = fma(-w, D, B.q[c]);
-                    const double e = pexp_lean(fmin(709.0, fmax(-745.0, x - Mrow[t])), thi, tlo);
-                    part[t * 32 + lane] += e;
-                }
-            }
-            __syncwarp();
-        } else {
-            if (!valid) return;
-            // phase 2: the surviving entries of this row, in column order (one exp each)
-            while (mask) {
-                const int c = __ffs(mask) - 1;
-                mask &= mask - 1u;
-                const double D = chunk_dist<COST, DP>(B, P, rp, i, j0, c, tile);
-                const double x = fma(-w, D, B.q[c]);
-                const double d = x - mx;
-                const double e = pexp_lean(fmax(-745.0, -fabs(d)), thi, tlo);
-                const bool up = d > 0.0;
-                sm = up ? fma(sm, e, 1.0) : sm + e;
-                mx = up ? x : mx;
-                jm = up ? (int)(j0 + c) : jm;
-            }
+            const double e1 = pexp_lean(fmax(-745.0, x1 - mx), thi, tlo);
+            const double e2 = pexp_lean(fmax(-745.0, x2 - mx), thi, tlo);
+            sm += two ? e1 + e2 : e1;
         }
     });
-    if constexpr (kWC<COST>) {
-        __syncwarp();
-        double t = 0.0;
-        for (int r = 0; r < 32; ++r) t += part[tid * 32 + ((r + lane) & 31)];
-        sm = t;
-    }
     if constexpr (COST == PC_SQTC) tc_teardown(tcs);
     skip_count(P, sk, nskip, jb, je);
     count_survivors(A.count_surv, 0, nsurv);
@@ -1087,7 +1007,8 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
     const int rb = bid % P.RB, sp = bid / P.RB;
     const long long i0 = (long long)rb * kPT, i = i0 + tid;
     const bool valid = i < P.M;
-    const long long jb = P.N * sp / P.S, je = P.N * (sp + 1) / P.S;
+    long long jb, je;
+    split_range(P.N, P.S, sp, jb, je);
     if constexpr (COST == PC_SQTC) tc_setup(tcs, P, i0);
     RowPt<COST, DP> rp;
     rp.load(P, i, valid);

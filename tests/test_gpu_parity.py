@@ -516,7 +516,7 @@ def test_tensor_core_cross_term_bit_identical(P, name, mk, monkeypatch):
     assert np.array_equal(a[5], b[5]) and np.array_equal(a[6], b[6])
 
 
-@pytest.mark.parametrize("name,mk", [("c1t", lambda: make("c1_rand1k", scale=0.3)),
+@pytest.mark.parametrize("name,mk", [("c1t", lambda: make("c1_rand1k", scale=0.3125)),
                                      ("rag_dense_t", lambda: ragged(301, 1030, 19)),
                                      ("tall", lambda: ragged(1030, 66, 20))])
 def test_tma_staged_dense_passes_bit_identical(P, name, mk, monkeypatch):
