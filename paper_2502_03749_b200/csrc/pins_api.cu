@@ -593,10 +593,11 @@ void fill_side(pins_workspace *ws, const pins_problem *pb, int o, const double *
 template <class K>
 size_t pass_smem(K kern, size_t bytes) {
     if (!bytes) return 0;
-    static bool done = false;
-    if (!done) {
+    static std::vector<const void *> done;          // per kernel (instantiations share a type)
+    const void *key = reinterpret_cast<const void *>(kern);
+    if (std::find(done.begin(), done.end(), key) == done.end()) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        done = true;
+        done.push_back(key);
     }
     return bytes;
 }
@@ -973,9 +974,9 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     PINS_TRY(ensure(ws->cgst, sizeof(double) * 16));
     // persistent arrays first, nnz-sized scratch last (offsets stay put as nnz changes)
     // comp hook tptr tnbr(2) deg fu fv1 fv2 tei tej tsrc(2) fs1 fs2 = 15 N, + rstart, ctr
-    const long long ni_fixed = 15 * N + 1 + kTreeMaxRounds + 1 + 8;
+    const long long ni_fixed = 15 * N + 1 + kTreeMaxRounds + 1 + 8 + (9 * N + 1);   // + pull lists
     const long long ni = ni_fixed + nnz;
-    const long long nd = 2 * N + N + 3 * N + 4 * N + 3 * N + 5 * N;   // tw, dcur, fc1/fc2/finv, r z p q, tval fw1 fw2, frec
+    const long long nd = 2 * N + N + 3 * N + 4 * N + 3 * N + 5 * N + 2 * N;   // tw, dcur, fc1/fc2/finv, r z p q, tval fw1 fw2, frec, lc
     const void *old_i = ws->tr_i.p, *old_d = ws->tr_d.p;
     PINS_TRY(ensure(ws->tr_i, sizeof(int) * ni));
     PINS_TRY(ensure(ws->tr_d, sizeof(double) * nd));
@@ -1021,6 +1022,12 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     A.tsrc = ip; ip += 2 * N;
     A.fs1 = ip; ip += N;
     A.fs2 = ip; ip += N;
+    A.cptr = ip; ip += N + 1;
+    A.cent = ip; ip += 2 * N;
+    A.ppos = ip; ip += 2 * N;
+    A.lu = ip; ip += 2 * N;
+    A.rpos = ip; ip += N;
+    A.cur = ip; ip += N;
     A.erow = ip;
     double *dp_ = ptr<double>(ws->tr_d);
     A.tw = dp_; dp_ += 2 * N;
@@ -1035,7 +1042,8 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     A.tval = dp_; dp_ += N;
     A.fw1 = dp_; dp_ += N;
     A.fw2 = dp_; dp_ += N;
-    A.frec = dp_;
+    A.frec = dp_; dp_ += 5 * N;
+    A.lc = dp_;
     unsigned char *bp = ptr<unsigned char>(ws->tr_u8);
     A.alive = bp; bp += N;
     A.sel = bp; bp += N;
@@ -1099,6 +1107,10 @@ int run_cg_tree_cluster(pins_workspace *ws, long long m, long long n, double mu,
     A.rstart = ws->tree_rstart;
     A.ctr = ws->tree_ctr;
     A.frec = ws->tree_frec;
+    A.fu = ws->tree_last.fu;
+    A.cptr = ws->tree_last.cptr;
+    A.lu = ws->tree_last.lu;
+    A.lc = ws->tree_last.lc;
     A.R = (int)((N + kTCW - 1) / kTCW);
     const size_t base = sizeof(double) * (size_t)N;
     const size_t budget = 220 * 1024;

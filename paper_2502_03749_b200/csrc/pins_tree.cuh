@@ -78,6 +78,15 @@ struct TreeArgs {
     double *fw1, *fw2;                 // [N] record slot weights
     int reuse;                         // 1: try the stored tree / schedule first
     int setup_only;                    // 1: stop after the factor is packed (cluster PCG follows)
+    // pull form of the elimination (deterministic, no atomics): for record q the records
+    // p eliminated next to it ("children": fv1[p] or fv2[p] is fu[q]), sorted by node
+    int *cptr;                         // [N + 1] child-list offsets per record
+    int *cent;                         // [2 N] child entries 2 p + slot (slot 0: v1, 1: v2)
+    int *ppos;                         // [2 N] list position of (p, slot)
+    int *lu;                           // [2 N] child node fu[p] of each entry
+    int *rpos;                         // [N] record of each node
+    int *cur;                          // [N] fill cursors
+    double *lc;                        // [2 N] forward multiplier of each entry (fc1 / fc2 of p)
 };
 
 __device__ __forceinline__ unsigned hash_prio(unsigned u, unsigned r) {
@@ -117,9 +126,6 @@ __device__ __forceinline__ Rec ldg_rec(const Rec *p) {
     return r;
 }
 
-// smem double atomic add (CAS loop; conflicts are rare: a node receives at most
-// one update per eliminated neighbour per round)
-__device__ __forceinline__ void sm_add(double *p, double v) { atomicAdd(p, v); }
 
 // block-wide exclusive scan of per-thread counts (kTT threads); returns the
 // thread's offset, *total gets the sum
@@ -181,35 +187,9 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
         }
         __syncthreads();
         if (s_flag) {
-            // numeric refactorisation on the stored schedule (push updates, round by round)
             nrounds = A.ctr[1];
-            for (int v = tid; v < N; v += kTT) A.dcur[v] = (v < m ? A.dr[v] : A.dc[v - m]) + mu;
             for (int k = tid; k <= nrounds; k += kTT) rs[k] = A.rstart[k];
             __syncthreads();
-            for (int rr = 0; rr < nrounds; ++rr) {
-                const int q1 = rs[rr + 1];
-                for (int q = rs[rr] + tid; q < q1; q += kTT) {
-                    const int s1 = A.fs1[q], s2 = A.fs2[q];
-                    double w1 = 0.0, w2 = 0.0;
-                    if (A.fv1[q] >= 0) {
-                        if (s1 >= 0) w1 = A.tval[s1];
-                        else { const int p0 = -s1 - 1; w1 = -A.fw1[p0] * A.fw2[p0] * A.finv[p0]; }
-                    }
-                    if (A.fv2[q] >= 0) {
-                        if (s2 >= 0) w2 = A.tval[s2];
-                        else { const int p0 = -s2 - 1; w2 = -A.fw1[p0] * A.fw2[p0] * A.finv[p0]; }
-                    }
-                    const double inv = 1.0 / A.dcur[A.fu[q]];
-                    A.fw1[q] = w1;
-                    A.fw2[q] = w2;
-                    A.fc1[q] = w1 * inv;
-                    A.fc2[q] = w2 * inv;
-                    A.finv[q] = inv;
-                    if (A.fv1[q] >= 0) atomicAdd(A.dcur + A.fv1[q], -w1 * w1 * inv);
-                    if (A.fv2[q] >= 0) atomicAdd(A.dcur + A.fv2[q], -w2 * w2 * inv);
-                }
-                __syncthreads();
-            }
             rebuilt = false;
         }
     }
@@ -414,7 +394,98 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
         __syncthreads();
     }
     if (tid == 0) A.ctr[1] = nrounds;
+    for (int k = tid; k <= nrounds; k += kTT) rs[k] = A.rstart[k];
+    __syncthreads();
+    // ---- child lists of the schedule (pull form): record q gathers from the records
+    // eliminated next to it; sorted by node id, so the order is independent of the
+    // (atomic) record numbering inside a round
+    {
+        const int nrec = rs[nrounds];
+        for (int q = tid; q < nrec; q += kTT) {
+            A.rpos[A.fu[q]] = q;
+            A.cur[q] = 0;
+        }
+        __syncthreads();
+        for (int p = tid; p < nrec; p += kTT) {
+            if (A.fv1[p] >= 0) atomicAdd(A.cur + A.rpos[A.fv1[p]], 1);
+            if (A.fv2[p] >= 0) atomicAdd(A.cur + A.rpos[A.fv2[p]], 1);
+        }
+        __syncthreads();
+        __shared__ int carry2;
+        if (tid == 0) { carry2 = 0; A.cptr[0] = 0; }
+        __syncthreads();
+        for (int base = 0; base < nrec; base += kTT) {
+            const int q = base + tid;
+            const int v = q < nrec ? A.cur[q] : 0;
+            int tot;
+            const int off = block_excl_scan(v, wsc, &tot);
+            if (q < nrec) A.cptr[q + 1] = carry2 + off + v;
+            __syncthreads();
+            if (tid == 0) carry2 += tot;
+            __syncthreads();
+        }
+        for (int q = tid; q < nrec; q += kTT) A.cur[q] = 0;
+        __syncthreads();
+        for (int p = tid; p < nrec; p += kTT)
+            for (int sl = 0; sl < 2; ++sl) {
+                const int v = sl ? A.fv2[p] : A.fv1[p];
+                if (v < 0) continue;
+                const int q = A.rpos[v];
+                A.cent[A.cptr[q] + atomicAdd(A.cur + q, 1)] = 2 * p + sl;
+            }
+        __syncthreads();
+        for (int q = tid; q < nrec; q += kTT) {
+            const int b = A.cptr[q], e = A.cptr[q + 1];
+            for (int k = b + 1; k < e; ++k) {           // insertion sort by child node
+                const int ck = A.cent[k], key = A.fu[ck >> 1];
+                int j = k - 1;
+                while (j >= b && A.fu[A.cent[j] >> 1] > key) { A.cent[j + 1] = A.cent[j]; --j; }
+                A.cent[j + 1] = ck;
+            }
+            for (int k = b; k < e; ++k) {
+                A.ppos[A.cent[k]] = k;
+                A.lu[k] = A.fu[A.cent[k] >> 1];
+            }
+        }
+        __syncthreads();
+    }
     }   // rebuild
+    // ---- numeric factor in pull form, round by round (deterministic, no atomics):
+    // d_u = diag_u - sum over children p of w_p^2 / d_p; slot weights from the tree
+    // edges (tval) or the fill edge of an earlier record (-w1 w2 / d)
+    for (int v = tid; v < N; v += kTT) A.dcur[v] = (v < m ? A.dr[v] : A.dc[v - m]) + mu;
+    __syncthreads();
+    for (int rr = 0; rr < nrounds; ++rr) {
+        const int q1 = rs[rr + 1];
+        for (int q = rs[rr] + tid; q < q1; q += kTT) {
+            const int u = A.fu[q];
+            double d = A.dcur[u];
+            for (int k = A.cptr[q]; k < A.cptr[q + 1]; ++k) {
+                const int ce = A.cent[k], p = ce >> 1;
+                const double w = (ce & 1) ? A.fw2[p] : A.fw1[p];
+                d -= w * w * A.finv[p];
+            }
+            const int s1 = A.fs1[q], s2 = A.fs2[q];
+            double w1 = 0.0, w2 = 0.0;
+            if (A.fv1[q] >= 0) {
+                if (s1 >= 0) w1 = A.tval[s1];
+                else { const int p0 = -s1 - 1; w1 = -A.fw1[p0] * A.fw2[p0] * A.finv[p0]; }
+            }
+            if (A.fv2[q] >= 0) {
+                if (s2 >= 0) w2 = A.tval[s2];
+                else { const int p0 = -s2 - 1; w2 = -A.fw1[p0] * A.fw2[p0] * A.finv[p0]; }
+            }
+            const double inv = 1.0 / d;
+            A.fw1[q] = w1;
+            A.fw2[q] = w2;
+            A.fc1[q] = w1 * inv;
+            A.fc2[q] = w2 * inv;
+            A.finv[q] = inv;
+            if (A.fv1[q] >= 0) A.lc[A.ppos[2 * q]] = w1 * inv;
+            if (A.fv2[q] >= 0) A.lc[A.ppos[2 * q + 1]] = w2 * inv;
+        }
+        __syncthreads();
+    }
     t_fac = clock64() - t_start - t_mst;
 
     // ---------------- 4. PCG on M with z = M_T^-1 r ----------------
@@ -458,6 +529,13 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
     const int warp_id = tid >> 5, lane_id = tid & 31;
     // in place on vs: forward elimination then back substitution (vs: r -> z)
     long long tpf = 0, tpw = 0, tpb = 0;
+    // forward elimination, pull form: record q's node gathers its children's final values
+    auto pull_row = [&](int q) {
+        const int u = A.fu[q];
+        double acc = vs[u];
+        for (int k = A.cptr[q]; k < A.cptr[q + 1]; ++k) acc = fma(-A.lc[k], vs[A.lu[k]], acc);
+        vs[u] = acc;
+    };
     auto precond_inplace = [&]() {
         const long long c0 = clock64();
         for (int rr = 0; rr < RW; ++rr) {
@@ -465,18 +543,12 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
             if (rr < R0) {                        // read-only path: loads may run ahead
 #pragma unroll 2
                 for (int q = q0r + tid; q < q1; q += kTT) {
-                    const Rec rc = ldg_rec(frec + q);
-                    const double yu = vs[rc.u];
-                    if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
-                    if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+                    pull_row(q);
                 }
             } else {
                 const Rec *src = tail - tbase;
                 for (int q = q0r + tid; q < q1; q += kTT) {
-                    const Rec rc = src[q];
-                    const double yu = vs[rc.u];
-                    if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
-                    if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+                    pull_row(q);
                 }
             }
             __syncthreads();
@@ -487,10 +559,7 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
             for (int rr = RW; rr < nrounds; ++rr) {
                 const int q = rs[rr] + lane_id;
                 if (q < rs[rr + 1]) {
-                    const Rec rc = src[q];
-                    const double yu = vs[rc.u];
-                    if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
-                    if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+                    pull_row(q);
                 }
                 __syncwarp();
             }

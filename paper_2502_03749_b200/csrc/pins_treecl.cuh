@@ -42,6 +42,8 @@ struct TreeCLArgs {
     const double *frec;                  // packed factor records (Rec, 40 B each)
     const int *rstart;                   // round boundaries
     const int *ctr;                      // [1] rounds
+    const int *fu, *cptr, *lu;           // pull form of the forward elimination (pins_tree.cuh)
+    const double *lc;
     int R;                               // unknowns per worker
     int tail_cap;                        // factor records cached in CTA 0's shared memory
     int use_x0;                          // 1: start from alpha x (x = the previous system's solution),
@@ -135,23 +137,24 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
     if (!worker)
         for (int q = tbase + tid; q < nrec; q += kCGT) tail[q - tbase] = frec[q];
     const int lane = tid & 31, warp = tid >> 5;
+    // forward elimination, pull form: record q's node gathers its children's final values
+    auto pull_row = [&](int q) {
+        const int u = A.fu[q];
+        double acc = vs[u];
+        for (int k = A.cptr[q]; k < A.cptr[q + 1]; ++k) acc = fma(-A.lc[k], vs[A.lu[k]], acc);
+        vs[u] = acc;
+    };
     // M_T^-1 in place on vs (CTA 0 only)
     auto tree_apply = [&]() {
         for (int rr = 0; rr < RW; ++rr) {
             const int q0r = rs[rr], q1 = rs[rr + 1];
             if (rr < R0) {
                 for (int q = q0r + tid; q < q1; q += kCGT) {
-                    const Rec rc = ldg_rec(frec + q);
-                    const double yu = vs[rc.u];
-                    if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
-                    if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+                    pull_row(q);
                 }
             } else {
                 for (int q = q0r + tid; q < q1; q += kCGT) {
-                    const Rec rc = tail[q - tbase];
-                    const double yu = vs[rc.u];
-                    if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
-                    if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+                    pull_row(q);
                 }
             }
             __syncthreads();
@@ -160,10 +163,7 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
             for (int rr = RW; rr < nrounds; ++rr) {
                 const int q = rs[rr] + lane;
                 if (q < rs[rr + 1]) {
-                    const Rec rc = tail[q - tbase];
-                    const double yu = vs[rc.u];
-                    if (rc.v1 >= 0) sm_add(vs + rc.v1, -rc.c1 * yu);
-                    if (rc.v2 >= 0) sm_add(vs + rc.v2, -rc.c2 * yu);
+                    pull_row(q);
                 }
                 __syncwarp();
             }
