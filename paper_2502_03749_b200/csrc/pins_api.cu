@@ -1114,9 +1114,11 @@ int run_cg_tree_cluster(pins_workspace *ws, long long m, long long n, double mu,
     A.R = (int)((N + kTCW - 1) / kTCW);
     const size_t base = sizeof(double) * (size_t)N;
     const size_t budget = 220 * 1024;
-    A.tail_cap = base < budget ? (int)((budget - base) / 40) : 0;
+    // per cached tail record: the 40-byte factor record, a list offset and two list entries
+    constexpr size_t kTailB = 40 + 4 + 2 * (4 + 8);
+    A.tail_cap = base + 64 < budget ? (int)((budget - base - 64) / kTailB) : 0;
     A.use_x0 = ws->x0_enable && ws->dir_valid && x == ptr<double>(ws->dir) && getenv("PINS_NO_X0") == nullptr;
-    const size_t smem = std::max<size_t>(base + (size_t)A.tail_cap * 40, sizeof(double) * 5 * (size_t)A.R);
+    const size_t smem = std::max<size_t>(base + (size_t)A.tail_cap * kTailB + 64, sizeof(double) * 5 * (size_t)A.R);
     static size_t configured = 0;
     if (smem > configured) {
         PINS_CUDA(cudaFuncSetAttribute(cg_tree_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -167,13 +167,35 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_schur
     Lc.heavy = heavy_c;
     if (tid == 0) { nh_r = 0; nh_c = 0; }
     __syncthreads();
-    for (int k = tid; k <= nr; k += kCGT) {
-        iptr_r[k] = (int)(A.rowptr[r0 + k] - rb);
-        if (k < nr && A.rowptr[r0 + k + 1] - A.rowptr[r0 + k] > kHeavy) heavy_r[atomicAdd(&nh_r, 1)] = k;
-    }
-    for (int k = tid; k <= nc; k += kCGT) {
-        iptr_c[k] = (int)(A.colptr[c0 + k] - cb);
-        if (k < nc && A.colptr[c0 + k + 1] - A.colptr[c0 + k] > kHeavy) heavy_c[atomicAdd(&nh_c, 1)] = k;
+    for (int k = tid; k <= nr; k += kCGT) iptr_r[k] = (int)(A.rowptr[r0 + k] - rb);
+    for (int k = tid; k <= nc; k += kCGT) iptr_c[k] = (int)(A.colptr[c0 + k] - cb);
+    // heavy lists in index order (deterministic work assignment): ordered compaction by
+    // warp ballots and a prefix over the warps of each block-sized batch
+    {
+        __shared__ int wcnt[kCGT / 32];
+        const int lane = tid & 31, warp = tid >> 5;
+        for (int side = 0; side < 2; ++side) {
+            const int len = side == 0 ? nr : nc;
+            const long long *pp = side == 0 ? A.rowptr + r0 : A.colptr + c0;
+            int *out = side == 0 ? heavy_r : heavy_c;
+            int base = 0;
+            for (int k0 = 0; k0 < len; k0 += kCGT) {
+                const int k = k0 + tid;
+                const bool h = k < len && pp[k + 1] - pp[k] > kHeavy;
+                const unsigned bal = __ballot_sync(0xffffffffu, h);
+                if (lane == 0) wcnt[warp] = __popc(bal);
+                __syncthreads();
+                int off = base, tot = 0;
+                for (int w2 = 0; w2 < kCGT / 32; ++w2) {
+                    if (w2 < warp) off += wcnt[w2];
+                    tot += wcnt[w2];
+                }
+                if (h) out[off + __popc(bal & ((1u << lane) - 1u))] = k;
+                base += tot;
+                __syncthreads();
+            }
+            if (tid == 0) (side == 0 ? nh_r : nh_c) = base;
+        }
     }
     const size_t need_r = (size_t)nzr * 12, need_c = (size_t)nzc * 12;
     const bool cache_r = need_r <= room;

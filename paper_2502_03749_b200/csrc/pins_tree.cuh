@@ -301,6 +301,26 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
             A.tw[pv] = w;
             A.tsrc[pv] = t;
         }
+    __syncthreads();
+    // adjacency lists in neighbour order (the atomic fill order is arbitrary): the
+    // contraction's choice of v1 / v2, hence every rounding downstream, is then fixed
+    for (int v = tid; v < N; v += kTT) {
+        const int b = A.tptr[v], e = A.tptr[v + 1];
+        for (int k = b + 1; k < e; ++k) {
+            const int nb = A.tnbr[k], sr = A.tsrc[k];
+            const double wk = A.tw[k];
+            int j = k - 1;
+            while (j >= b && A.tnbr[j] > nb) {
+                A.tnbr[j + 1] = A.tnbr[j];
+                A.tw[j + 1] = A.tw[j];
+                A.tsrc[j + 1] = A.tsrc[j];
+                --j;
+            }
+            A.tnbr[j + 1] = nb;
+            A.tw[j + 1] = wk;
+            A.tsrc[j + 1] = sr;
+        }
+    }
     for (int v = tid; v < N; v += kTT) {
         alive[v] = 1;
         A.dcur[v] = (v < m ? A.dr[v] : A.dc[v - m]) + mu;

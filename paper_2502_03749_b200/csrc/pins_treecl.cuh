@@ -127,18 +127,38 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
     for (int k = tid; k <= nrounds; k += kCGT) rs[k] = A.rstart[k];
     const Rec *frec = reinterpret_cast<const Rec *>(A.frec);
     Rec *tail = reinterpret_cast<Rec *>(dyn + 8 * (size_t)N);
+    // the tail's forward (pull) lists: offsets, child nodes, multipliers
+    int *tl_ptr = reinterpret_cast<int *>(tail + A.tail_cap);
+    int *tl_u = tl_ptr + A.tail_cap + 1;
+    double *tl_c = reinterpret_cast<double *>(
+        (reinterpret_cast<uintptr_t>(tl_u + 2 * A.tail_cap) + 7) & ~uintptr_t(7));
     __syncthreads();
     const int nrec = rs[nrounds];
     int R0 = nrounds;
-    while (R0 > 0 && nrec - rs[R0 - 1] <= A.tail_cap) --R0;
+    while (R0 > 0 && nrec - rs[R0 - 1] <= A.tail_cap && A.cptr[nrec] - A.cptr[rs[R0 - 1]] <= 2 * A.tail_cap) --R0;
     const int tbase = rs[R0];
+    const int kbase = A.cptr[tbase];
     int RW = nrounds;
     while (RW > R0 && rs[RW] - rs[RW - 1] <= 32) --RW;
-    if (!worker)
+    if (!worker) {
         for (int q = tbase + tid; q < nrec; q += kCGT) tail[q - tbase] = frec[q];
+        for (int q = tbase + tid; q <= nrec; q += kCGT) tl_ptr[q - tbase] = A.cptr[q] - kbase;
+        for (int k = kbase + tid; k < A.cptr[nrec]; k += kCGT) {
+            tl_u[k - kbase] = A.lu[k];
+            tl_c[k - kbase] = A.lc[k];
+        }
+    }
     const int lane = tid & 31, warp = tid >> 5;
     // forward elimination, pull form: record q's node gathers its children's final values
+    // (lists of the early rounds from global memory, of the cached tail from shared memory)
     auto pull_row = [&](int q) {
+        if (q >= tbase) {
+            const int u = tail[q - tbase].u;
+            double acc = vs[u];
+            for (int k = tl_ptr[q - tbase]; k < tl_ptr[q - tbase + 1]; ++k) acc = fma(-tl_c[k], vs[tl_u[k]], acc);
+            vs[u] = acc;
+            return;
+        }
         const int u = A.fu[q];
         double acc = vs[u];
         for (int k = A.cptr[q]; k < A.cptr[q + 1]; ++k) acc = fma(-A.lc[k], vs[A.lu[k]], acc);
