@@ -189,8 +189,8 @@ int pins_residuals(pins_workspace *ws, const pins_problem *pb, const double *phi
 
 /* LP certificate of the plan X~(f,g) at centre (phi, psi, s) (reading R11,
  * DESIGN.md §3; LP duality of Eq. (1)): evaluation with the
- * plan block sparsified at tau = prm->theta/(m n); maximum-weight spanning
- * forest of that support (the LP optimum is a vertex, whose
+ * plan block sparsified at tau = 1e-12/(m n) (prm is not used for it); the
+ * maximum-weight spanning forest of that support (the LP optimum is a vertex, whose
  * support is a forest); tree duals u_i + v_j = C_ij on the forest; row then
  * column c-transforms u_i = min_j C_ij - v_j, v_j = min_i C_ij - u_i (dual
  * feasible by construction); the entropic duals are the fallback candidate.

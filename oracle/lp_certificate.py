@@ -16,7 +16,9 @@ above (up to X's own marginal residual).  The duals are built in three steps,
 each a plain definition:
 
 1. basis: a maximum-weight spanning forest T of the sparsified support graph
-   of X~ (rows and columns are nodes, kept entries X~_ij >= tau are edges).
+   of X~ (rows and columns are nodes, kept entries X~_ij >= tau are edges;
+   the GPU uses tau = 1e-12/(m n), far below the Newton threshold, so basic
+   edges with tiny flows stay in the graph).
    PAPER.md Thm 4.3 proof (lines 362): the LP optimum is a vertex of the
    transport polytope; a vertex's support is a forest of the bipartite graph
    (a spanning tree when non-degenerate), and PINS' plans concentrate on it

@@ -1285,11 +1285,18 @@ int certify_tree(pins_workspace *ws, const pins_problem *pb, const EvalOut &cur,
 // forest -> tree duals -> row / column c-transforms; the entropic duals
 // ((f + phi)/s, (g + psi - eta)/s) are the second candidate; the larger
 // certified bound wins.  Certified duals -> ws->cbu / cbv.
+// Support of the certificate: entries X~_ij >= kThetaCert/(m n) -- far below the
+// Newton sparsification threshold, so that basic edges carrying tiny flows (which
+// connect otherwise separate components) are part of the graph (reading R11).
+constexpr double kThetaCert = 1e-12;
+
 int certify(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi, double s,
-            const double *f, const double *g, const EvalOut &cur, bool want_dual_inf, CertOut *co,
-            cudaStream_t st, double target_gap = -INFINITY) {
+            const double *f, const double *g, bool want_dual_inf, CertOut *co, cudaStream_t st,
+            double target_gap = -INFINITY) {
     *co = CertOut();
     const long long m = pb->m, n = pb->n, N = m + n;
+    EvalOut cur;
+    PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, kThetaCert / ((double)m * (double)n), false, st, &cur));
     PINS_TRY(prepare(ws, pb));
     for (DevBuf *b : {&ws->cu0, &ws->cu1, &ws->cbu, &ws->crow}) PINS_TRY(ensure(*b, sizeof(double) * std::max(m, n)));
     for (DevBuf *b : {&ws->cv0, &ws->cv1, &ws->cbv}) PINS_TRY(ensure(*b, sizeof(double) * n));
@@ -1649,11 +1656,8 @@ extern "C" int pins_lp_certificate(pins_workspace *ws, const pins_problem *pb, c
     invalidate_problem(ws);
     PINS_ARG(phi && psi && f && g && s > 0.0, "phi, psi, f, g, s > 0");
     cudaStream_t st = (cudaStream_t)stream;
-    const double tau = prm->theta / ((double)pb->m * (double)pb->n);
-    EvalOut e;
-    PINS_TRY(run_eval(ws, pb, phi, psi, s, f, g, tau, false, st, &e));
     CertOut co;
-    PINS_TRY(certify(ws, pb, phi, psi, s, f, g, e, true, &co, st));
+    PINS_TRY(certify(ws, pb, phi, psi, s, f, g, true, &co, st));
     if (u) PINS_CUDA(cudaMemcpyAsync(u, ws->cbu.p, sizeof(double) * pb->m, cudaMemcpyDeviceToDevice, st));
     if (v) PINS_CUDA(cudaMemcpyAsync(v, ws->cbv.p, sizeof(double) * pb->n, cudaMemcpyDeviceToDevice, st));
     PINS_CUDA(cudaStreamSynchronize(st));
@@ -1797,7 +1801,7 @@ static int solve_core(pins_workspace *ws, const pins_problem *pb, const pins_par
             halving_seen = halving_seen || halving;
             if (trigger && cur.gnorm <= prm->newton_tol) {
                 const double target = prm->outer_tol * std::fabs(cur.cost);
-                PINS_TRY(certify(ws, pb, phi, psi, s, f, g, cur, false, &cert, st, target));
+                PINS_TRY(certify(ws, pb, phi, psi, s, f, g, false, &cert, st, target));
                 cert_k = k;
                 ++n_certs;
                 if (cert_trace)     // dev instrumentation (PINS_CERT_TRACE=1)
@@ -1812,7 +1816,7 @@ static int solve_core(pins_workspace *ws, const pins_problem *pb, const pins_par
             stop = outer_converged(objs, prm);
         }
         if ((stop || last) && cert_k != k) {        // the returned plan's certificate (report)
-            PINS_TRY(certify(ws, pb, phi, psi, s, f, g, cur, false, &cert, st));
+            PINS_TRY(certify(ws, pb, phi, psi, s, f, g, false, &cert, st));
             cert_k = k;
             ++n_certs;
         }

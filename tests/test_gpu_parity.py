@@ -320,7 +320,7 @@ def test_lp_certificate_matches_oracle(P, name, mk, k):
     ws = P.Workspace()
     cg = P.lp_certificate(ws, pb, prm, T(phi), T(psi), s, T(f), T(g))
     Pg = H(P.plan(pb, T(phi), T(psi), s, T(f), T(g)))
-    tau = prm.theta / (w.m * w.n)
+    tau = 1e-12 / (w.m * w.n)                    # the certificate's support (pins.h)
     o = lc.certify(C, w.a, w.b, Pg, tau, duals0=((f + phi) / s, (g + psi - w.eta) / s))
     assert cg["tree_edges"] == len(o["forest"])
     cmax = np.abs(C).max()
