@@ -75,7 +75,7 @@ typedef struct pins_params {
     double newton_tol;       /* Newton phase: ||grad P||_1 threshold      (1e-8)  */
     double theta;            /* sparsify: keep X~_ij >= theta/(m n)       (1e-4)  */
     double cg_tol;           /* CG relative-residual floor                (1e-6)  */
-    double cg_forcing;       /* rtol = clamp(cg_forcing*newton_tol/||g||_1, cg_tol, 0.5) (0.1) */
+    double cg_forcing;       /* rtol = clamp(cg_forcing*newton_tol/||g||_1, cg_tol, 0.5) (0.5) */
     int32_t cg_maxit;        /* (1000) */
     double mu_rel;           /* damping mu = mu_rel * max diagonal        (1e-10) */
     double armijo_c;         /* (1e-4) */

@@ -191,7 +191,7 @@ class Params:
     newton_tol: float = 1e-8      # A.2 "absolute error threshold of 1e-8"
     theta: float = 1e-4           # sparsify threshold tau = theta/(m n) (reading R3)
     cg_tol: float = 1e-6          # floor of the CG relative tolerance
-    cg_forcing: float = 0.1       # reading R5: rtol = clamp(cg_forcing*newton_tol/||grad||_1, cg_tol, 0.5)
+    cg_forcing: float = 0.5       # reading R5: rtol = clamp(cg_forcing*newton_tol/||grad||_1, cg_tol, 0.5)
     cg_maxit: int = 1000
     mu_rel: float = 1e-10         # Tikhonov damping relative to max diagonal (reading R5)
     armijo_c: float = 1e-4        # reading R4

@@ -210,7 +210,7 @@ extern "C" void pins_default_params(pins_params *p) {
     p->newton_tol = 1e-8;
     p->theta = 1e-4;
     p->cg_tol = 1e-6;
-    p->cg_forcing = 0.1;
+    p->cg_forcing = 0.5;
     p->cg_maxit = 1000;
     p->mu_rel = 1e-10;
     p->armijo_c = 1e-4;
