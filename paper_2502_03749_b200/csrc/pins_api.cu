@@ -974,9 +974,9 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     PINS_TRY(ensure(ws->cgst, sizeof(double) * 16));
     // persistent arrays first, nnz-sized scratch last (offsets stay put as nnz changes)
     // comp hook tptr tnbr(2) deg fu fv1 fv2 tei tej tsrc(2) fs1 fs2 = 15 N, + rstart, ctr
-    const long long ni_fixed = 15 * N + 1 + kTreeMaxRounds + 1 + 8 + (9 * N + 1);   // + pull lists
+    const long long ni_fixed = 15 * N + 1 + kTreeMaxRounds + 1 + 8 + (11 * N + 1);   // + pull lists
     const long long ni = ni_fixed + nnz;
-    const long long nd = 2 * N + N + 3 * N + 4 * N + 3 * N + 5 * N + 2 * N;   // tw, dcur, fc1/fc2/finv, r z p q, tval fw1 fw2, frec, lc
+    const long long nd = 4 * N + 2 * N + N + 3 * N + 4 * N + 3 * N + 5 * N;   // pull entries, tw, dcur, fc1/fc2/finv, r z p q, tval fw1 fw2, frec
     const void *old_i = ws->tr_i.p, *old_d = ws->tr_d.p;
     PINS_TRY(ensure(ws->tr_i, sizeof(int) * ni));
     PINS_TRY(ensure(ws->tr_d, sizeof(double) * nd));
@@ -1007,6 +1007,7 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     A.b = b;
     A.st = ptr<double>(ws->cgst);
     int *ip = ptr<int>(ws->tr_i);
+    A.pk = reinterpret_cast<int4 *>(ip); ip += 4 * N;     // 16-byte aligned: first in the pool
     A.comp = ip; ip += N;
     A.hook = ip; ip += N;
     A.tptr = ip; ip += N + 1;
@@ -1025,11 +1026,11 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     A.cptr = ip; ip += N + 1;
     A.cent = ip; ip += 2 * N;
     A.ppos = ip; ip += 2 * N;
-    A.lu = ip; ip += 2 * N;
     A.rpos = ip; ip += N;
     A.cur = ip; ip += N;
     A.erow = ip;
     double *dp_ = ptr<double>(ws->tr_d);
+    A.pe = reinterpret_cast<PullE *>(dp_); dp_ += 4 * N;  // 16-byte aligned: first in the pool
     A.tw = dp_; dp_ += 2 * N;
     A.dcur = dp_; dp_ += N;
     A.fc1 = dp_; dp_ += N;
@@ -1042,8 +1043,7 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     A.tval = dp_; dp_ += N;
     A.fw1 = dp_; dp_ += N;
     A.fw2 = dp_; dp_ += N;
-    A.frec = dp_; dp_ += 5 * N;
-    A.lc = dp_;
+    A.frec = dp_;
     unsigned char *bp = ptr<unsigned char>(ws->tr_u8);
     A.alive = bp; bp += N;
     A.sel = bp; bp += N;
@@ -1107,15 +1107,14 @@ int run_cg_tree_cluster(pins_workspace *ws, long long m, long long n, double mu,
     A.rstart = ws->tree_rstart;
     A.ctr = ws->tree_ctr;
     A.frec = ws->tree_frec;
-    A.fu = ws->tree_last.fu;
     A.cptr = ws->tree_last.cptr;
-    A.lu = ws->tree_last.lu;
-    A.lc = ws->tree_last.lc;
+    A.pk = ws->tree_last.pk;
+    A.pe = ws->tree_last.pe;
     A.R = (int)((N + kTCW - 1) / kTCW);
     const size_t base = sizeof(double) * (size_t)N;
     const size_t budget = 220 * 1024;
     // per cached tail record: the 40-byte factor record, a list offset and two list entries
-    constexpr size_t kTailB = 40 + 4 + 2 * (4 + 8);
+    constexpr size_t kTailB = 40 + 16 + 2 * 16;      // record, pull header, two pull entries
     A.tail_cap = base + 64 < budget ? (int)((budget - base - 64) / kTailB) : 0;
     A.use_x0 = ws->x0_enable && ws->dir_valid && x == ptr<double>(ws->dir) && getenv("PINS_NO_X0") == nullptr;
     const size_t smem = std::max<size_t>(base + (size_t)A.tail_cap * kTailB + 64, sizeof(double) * 5 * (size_t)A.R);

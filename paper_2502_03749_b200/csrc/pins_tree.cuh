@@ -33,6 +33,12 @@
 namespace pins {
 
 constexpr int kTT = 1024;              // threads of the tree-CG CTA
+
+// one entry of a record's pull list: a child's node and its forward multiplier
+struct alignas(16) PullE {
+    int node, pad;
+    double coef;
+};
 constexpr int kTreeMaxRounds = 256;
 
 struct TreeArgs {
@@ -83,10 +89,10 @@ struct TreeArgs {
     int *cptr;                         // [N + 1] child-list offsets per record
     int *cent;                         // [2 N] child entries 2 p + slot (slot 0: v1, 1: v2)
     int *ppos;                         // [2 N] list position of (p, slot)
-    int *lu;                           // [2 N] child node fu[p] of each entry
+    int4 *pk;                          // [N] per record: {node, first entry, entries, 0}
     int *rpos;                         // [N] record of each node
     int *cur;                          // [N] fill cursors
-    double *lc;                        // [2 N] forward multiplier of each entry (fc1 / fc2 of p)
+    struct PullE *pe;                  // [2 N] entries {child node, multiplier fc1 / fc2 of p}
 };
 
 __device__ __forceinline__ unsigned hash_prio(unsigned u, unsigned r) {
@@ -464,8 +470,10 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
             }
             for (int k = b; k < e; ++k) {
                 A.ppos[A.cent[k]] = k;
-                A.lu[k] = A.fu[A.cent[k] >> 1];
+                A.pe[k].node = A.fu[A.cent[k] >> 1];
+                A.pe[k].pad = 0;
             }
+            A.pk[q] = make_int4(A.fu[q], b, e - b, 0);
         }
         __syncthreads();
     }
@@ -501,8 +509,8 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
             A.fc1[q] = w1 * inv;
             A.fc2[q] = w2 * inv;
             A.finv[q] = inv;
-            if (A.fv1[q] >= 0) A.lc[A.ppos[2 * q]] = w1 * inv;
-            if (A.fv2[q] >= 0) A.lc[A.ppos[2 * q + 1]] = w2 * inv;
+            if (A.fv1[q] >= 0) A.pe[A.ppos[2 * q]].coef = w1 * inv;
+            if (A.fv2[q] >= 0) A.pe[A.ppos[2 * q + 1]].coef = w2 * inv;
         }
         __syncthreads();
     }
@@ -551,10 +559,13 @@ __global__ void __launch_bounds__(kTT, 1) tree_pcg_kernel(TreeArgs A) {
     long long tpf = 0, tpw = 0, tpb = 0;
     // forward elimination, pull form: record q's node gathers its children's final values
     auto pull_row = [&](int q) {
-        const int u = A.fu[q];
-        double acc = vs[u];
-        for (int k = A.cptr[q]; k < A.cptr[q + 1]; ++k) acc = fma(-A.lc[k], vs[A.lu[k]], acc);
-        vs[u] = acc;
+        const int4 h = A.pk[q];
+        double acc = vs[h.x];
+        for (int k = h.y; k < h.y + h.z; ++k) {
+            const PullE e = A.pe[k];
+            acc = fma(-e.coef, vs[e.node], acc);
+        }
+        vs[h.x] = acc;
     };
     auto precond_inplace = [&]() {
         const long long c0 = clock64();

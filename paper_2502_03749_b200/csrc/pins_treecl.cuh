@@ -42,8 +42,9 @@ struct TreeCLArgs {
     const double *frec;                  // packed factor records (Rec, 40 B each)
     const int *rstart;                   // round boundaries
     const int *ctr;                      // [1] rounds
-    const int *fu, *cptr, *lu;           // pull form of the forward elimination (pins_tree.cuh)
-    const double *lc;
+    const int *cptr;                     // pull form of the forward elimination (pins_tree.cuh)
+    const int4 *pk;
+    const PullE *pe;
     int R;                               // unknowns per worker
     int tail_cap;                        // factor records cached in CTA 0's shared memory
     int use_x0;                          // 1: start from alpha x (x = the previous system's solution),
@@ -127,11 +128,10 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
     for (int k = tid; k <= nrounds; k += kCGT) rs[k] = A.rstart[k];
     const Rec *frec = reinterpret_cast<const Rec *>(A.frec);
     Rec *tail = reinterpret_cast<Rec *>(dyn + 8 * (size_t)N);
-    // the tail's forward (pull) lists: offsets, child nodes, multipliers
-    int *tl_ptr = reinterpret_cast<int *>(tail + A.tail_cap);
-    int *tl_u = tl_ptr + A.tail_cap + 1;
-    double *tl_c = reinterpret_cast<double *>(
-        (reinterpret_cast<uintptr_t>(tl_u + 2 * A.tail_cap) + 7) & ~uintptr_t(7));
+    // the tail's forward (pull) lists: record headers and entries
+    int4 *tl_h = reinterpret_cast<int4 *>(
+        (reinterpret_cast<uintptr_t>(tail + A.tail_cap) + 15) & ~uintptr_t(15));
+    PullE *tl_e = reinterpret_cast<PullE *>(tl_h + A.tail_cap);
     __syncthreads();
     const int nrec = rs[nrounds];
     int R0 = nrounds;
@@ -141,28 +141,27 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
     int RW = nrounds;
     while (RW > R0 && rs[RW] - rs[RW - 1] <= 32) --RW;
     if (!worker) {
-        for (int q = tbase + tid; q < nrec; q += kCGT) tail[q - tbase] = frec[q];
-        for (int q = tbase + tid; q <= nrec; q += kCGT) tl_ptr[q - tbase] = A.cptr[q] - kbase;
-        for (int k = kbase + tid; k < A.cptr[nrec]; k += kCGT) {
-            tl_u[k - kbase] = A.lu[k];
-            tl_c[k - kbase] = A.lc[k];
+        for (int q = tbase + tid; q < nrec; q += kCGT) {
+            tail[q - tbase] = frec[q];
+            int4 h = A.pk[q];
+            h.y -= kbase;
+            tl_h[q - tbase] = h;
         }
+        for (int k = kbase + tid; k < A.cptr[nrec]; k += kCGT) tl_e[k - kbase] = A.pe[k];
     }
     const int lane = tid & 31, warp = tid >> 5;
     // forward elimination, pull form: record q's node gathers its children's final values
     // (lists of the early rounds from global memory, of the cached tail from shared memory)
     auto pull_row = [&](int q) {
-        if (q >= tbase) {
-            const int u = tail[q - tbase].u;
-            double acc = vs[u];
-            for (int k = tl_ptr[q - tbase]; k < tl_ptr[q - tbase + 1]; ++k) acc = fma(-tl_c[k], vs[tl_u[k]], acc);
-            vs[u] = acc;
-            return;
+        const bool t = q >= tbase;
+        const int4 h = t ? tl_h[q - tbase] : A.pk[q];
+        const PullE *E = t ? tl_e : A.pe;
+        double acc = vs[h.x];
+        for (int k = h.y; k < h.y + h.z; ++k) {
+            const PullE e = E[k];
+            acc = fma(-e.coef, vs[e.node], acc);
         }
-        const int u = A.fu[q];
-        double acc = vs[u];
-        for (int k = A.cptr[q]; k < A.cptr[q + 1]; ++k) acc = fma(-A.lc[k], vs[A.lu[k]], acc);
-        vs[u] = acc;
+        vs[h.x] = acc;
     };
     // M_T^-1 in place on vs (CTA 0 only)
     auto tree_apply = [&]() {
