@@ -460,8 +460,11 @@ def test_solve_small_scale_reaches_exact_lp(P, name, scale):
     assert r["kkt"] <= 1e-8
     assert abs(r["obj"] - ex["obj"]) <= 1e-7 * abs(ex["obj"])
     tr = np.array(r["trace"])
-    # Thm 4.1: <C, X^{k+1}> <= <C, X^k> (inexact solves: 1e-10 slack)
-    assert np.all(np.diff(tr) <= 1e-10 * abs(tr[0]))
+    # Thm 4.1: <C, X^{k+1}> <= <C, X^k> for exact subproblem solves.  The
+    # solves stop at ||grad P^k||_1 <= newton_tol, i.e. each plan's marginals are off by at
+    # most newton_tol in l1, which moves <C, X> by at most newton_tol max C: slack 2 newton_tol max C
+    cmax = po.cost_matrix(w).max()
+    assert np.all(np.diff(tr) <= 2 * BENCH["newton_tol"] * cmax)
 
 
 def test_edge_cases(P):
