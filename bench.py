@@ -396,9 +396,14 @@ def hbm_section(pins, peaks):
     pins.prof_enable(True)
     nsw = 20
     pins.sinkhorn(ws, pb, phi, psi, s, f, g, 0.0, nsw)
-    ev = pins.evaluate(ws, pb, phi, psi, s, f, g, tau=1e-4 / (w.m * w.n))
+    pins.evaluate(ws, pb, phi, psi, s, f, g, tau=0.0)        # sums only: the C stream
     pins.prof_enable(False)
     prof = pins.prof_read()
+    pins.prof_reset()
+    pins.prof_enable(True)
+    ev = pins.evaluate(ws, pb, phi, psi, s, f, g, tau=1e-4 / (w.m * w.n))   # + sparsify
+    pins.prof_enable(False)
+    prof_sp = pins.prof_read()
     byt = 8.0 * w.m * w.n
     for c in ("sweep_row", "sweep_col", "eval"):
         L, ms = prof[c]["launches"], prof[c]["ms"]
@@ -409,8 +414,15 @@ def hbm_section(pins, peaks):
         out[f"dense_{c}"] = {"launches": L, "avg_launch_us": ms / L * 1e3, "achieved": gbs, "peak": peak,
                              "unit": "GB/s", "frac": gbs / peak, "bytes_per_launch": mult * byt,
                              "survivors_per_launch": prof[c]["work"] / L if c != "sweep_col" else None}
+    L, ms = prof_sp["eval"]["launches"], prof_sp["eval"]["ms"]
+    if L:
+        gbs = 2.0 * byt / (ms / L / 1e3) / 1e9
+        out["dense_eval_sparsify"] = {"launches": L, "avg_launch_us": ms / L * 1e3, "achieved": gbs, "peak": peak,
+                                      "unit": "GB/s", "frac": gbs / peak, "bytes_per_launch": 2.0 * byt,
+                                      "kept_entries": ev["nnz"]}
     out["dense_config"] = ("c3_gmm10k cost materialised densely (10^4 x 10^4 fp64, 800 MB), k = 0, "
-                           f"{nsw} Sinkhorn sweeps + 1 sum pass (nnz {ev['nnz']})")
+                           f"{nsw} Sinkhorn sweeps, 1 sum pass (sums only), 1 sum pass with sparsification "
+                           f"(nnz {ev['nnz']})")
     del C, pb, ws
     torch.cuda.empty_cache()
     # (2) SpMV: random support with 2.4e7 entries (m = n = 10^4, ~12 % dense -- the k = 1
