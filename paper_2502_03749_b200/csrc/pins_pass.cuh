@@ -722,7 +722,7 @@ __device__ __forceinline__ double chunk_dist(const Buf<COST, DP> &B, const PassS
     } else if constexpr (COST == PC_DENSE_COL_T) { // {128 x 32} box, column = thread
         return *reinterpret_cast<const double *>(tile + c * (kPT * 8) + threadIdx.x * 8);
     } else if constexpr (COST == PC_DENSE_ROW) return B.tile[c * (kPT + 1) + threadIdx.x];
-    else if constexpr (COST == PC_DENSE_COL) return __ldg(P.C + (j0 + c) * P.ldc + i);
+    else if constexpr (COST == PC_DENSE_COL) return j0 + c < P.N ? __ldg(P.C + (j0 + c) * P.ldc + i) : 0.0;
     else if constexpr (COST == PC_SQTC) return 0.0;
     else return rp.dist(B, c);
 }
@@ -830,8 +830,10 @@ __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSid
                 if constexpr (kDv<COST>) Dv[c] = Df;
             }
             const float v = fmaf(-w_lo, Df, qsv[j]);
-            vmx = c < nc ? fmaxf(vmx, v) : vmx;
-            mask |= (c < nc && v > thr32) ? (1u << c) : 0u;
+            // columns c >= nc of a partial chunk are staged with q = -inf, so v = -inf there:
+            // no per-entry range test is needed
+            vmx = fmaxf(vmx, v);
+            mask |= (v > thr32) ? (1u << c) : 0u;
         }
     }
     return mask;
