@@ -12,6 +12,7 @@ cap() {   # tag mode regex skip
   if [ -n "$5" ]; then ncu -i /tmp/prof_$tag.ncu-rep --page source --csv --print-source sass 2>&1 | gzip > gpurun_out/ncu_r2_${tag}_src_sass.csv.gz; fi
 }
 cap sweep sweep 'lse_pass' 40 src
+cap eval eval 'sum_pass' 5
 cap denserow dense 'lse_pass_kernel<7' 6
 cap densecol dense 'lse_pass_kernel<8' 6
 cap densesum dense 'sum_pass' 0
