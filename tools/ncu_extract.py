@@ -10,7 +10,8 @@ import csv, glob, gzip, json, os, sys
 SRC = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-         "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3, "second": 1e6}
+         "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3, "second": 1e6,
+         "us": 1.0, "ns": 1e-3, "ms": 1e3, "s": 1e6}
 WANT = {"duration_us": "gpu__time_duration.sum", "dram_read_B": "dram__bytes_read.sum",
         "dram_write_B": "dram__bytes_write.sum", "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "occupancy_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",

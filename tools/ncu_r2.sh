@@ -13,8 +13,8 @@ cap() {   # tag mode regex skip
 }
 cap sweep sweep 'lse_pass' 40 src
 cap eval eval 'sum_pass' 5
-cap denserow dense 'lse_pass_kernel<7' 6
-cap densecol dense 'lse_pass_kernel<8' 6
+cap denserow dense 'lse_pass_kernel<\(int\)7' 6
+cap densecol dense 'lse_pass_kernel<\(int\)8' 6
 cap densesum dense 'sum_pass' 0
 cap treecl late 'cg_tree_cluster' 150
 cap treefac late 'tree_pcg' 150
