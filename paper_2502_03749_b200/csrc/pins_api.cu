@@ -175,7 +175,7 @@ struct pins_workspace {
     // v2 dense passes
     SideBufs sb[2];
     DevBuf x32, y32, x64, y64, nx32, ny32, xh, yh, pinfo, ctl, gticket, pst, tol;
-    DevBuf sk_gam[4], sk_tref[4], sk_qref[4], skst;   // chunk-skip certificates: (LSE, SUM) x orientation
+    DevBuf sk_gam[4], sk_gamD[4], sk_tref[4], sk_qref[4], skst;   // chunk-skip certificates: (LSE, SUM) x orientation
     const void *key_C = nullptr, *key_x = nullptr, *key_y = nullptr;
     long long key_m = -1, key_n = -1, key_ldc = -1;
     int key_kind = -1, key_d = -1;
@@ -188,6 +188,8 @@ struct pins_workspace {
     bool tree_valid = false;
     long long tree_N = -1;
     int tree_last_its = 0, tree_backoff = 0;
+    bool tree_newton = false;          // the stored factor is a Newton system's (not a certificate's)
+    int tree_stale = 0;                // Newton systems solved since the factor was computed
     const int *tree_rstart = nullptr, *tree_ctr = nullptr;
     const double *tree_frec = nullptr;
     TreeArgs tree_last;                // arguments of the last tree build (certificate replay)
@@ -395,6 +397,7 @@ void invalidate_problem(pins_workspace *ws) {
     ws->key_m = ws->key_n = ws->key_ldc = -1;
     ws->key_kind = ws->key_d = -1;
     ws->tree_valid = false;
+    ws->tree_newton = false;
     ws->dir_valid = false;
     ws->tree_backoff = 0;
 }
@@ -409,8 +412,10 @@ int prepare_pass(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
     for (int q = 0; q < 2; ++q) {
         const long long M = q == 0 ? m : n, N = q == 0 ? n : m;
         const int RB = (int)((M + kPT - 1) / kPT);
-        // column splits: ~8 CTAs of 128 threads per SM per side, splits >= kCC columns
-        long long S = (8LL * ws->nsm + RB - 1) / RB;
+        // column splits: ~14 CTAs of 128 threads per SM per side (about 3 waves at the
+        // half-sweep's 5 CTAs per SM: measured on c3, 4.19 s vs 4.44 s at 8), splits >= kCC columns
+        static const double split_f = getenv("PINS_SPLIT_F") ? atof(getenv("PINS_SPLIT_F")) : 14.4;
+        long long S = ((long long)(split_f * ws->nsm) + RB - 1) / RB;
         S = std::max(1LL, std::min(S, std::max(1LL, N / kCC)));
         ws->S[q] = (int)S;
         SideBufs &B = ws->sb[q];
@@ -506,6 +511,7 @@ int prepare_pass(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
             const long long RB = (M + kPT - 1) / kPT, S = ws->S[o];
             const long long cps = ((N + S - 1) / S + kCC - 1) / kCC + 1;
             PINS_TRY(ensure(ws->sk_gam[q], sizeof(float) * RB * S * cps * 4));
+            PINS_TRY(ensure(ws->sk_gamD[q], sizeof(float) * RB * S * cps * 4));
             PINS_TRY(ensure(ws->sk_tref[q], sizeof(float) * M));
             PINS_TRY(ensure(ws->sk_qref[q], sizeof(float) * N));
         }
@@ -524,6 +530,7 @@ void set_skip(pins_workspace *ws, PassSide &P, int q) {
     if (!P.skipk) return;
     P.cps = (int)(((P.N + P.S - 1) / P.S + kCC - 1) / kCC + 1);
     P.gam = ptr<float>(ws->sk_gam[q]);
+    P.gamD = ptr<float>(ws->sk_gamD[q]);
     P.tref = ptr<float>(ws->sk_tref[q]);
     P.qref = ptr<float>(ws->sk_qref[q]);
     P.skst = ptr<int>(ws->skst) + 16 * q;
@@ -1070,6 +1077,8 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     LAUNCH(PINS_PROF_CG, st, tree_pcg_kernel<<<1, kTT, smem, st>>>(A));
     PINS_CUDA(cudaGetLastError());
     ws->tree_valid = true;
+    ws->tree_newton = wval == nullptr;
+    ws->tree_stale = 0;
     ws->tree_N = N;
     return PINS_OK;
 }
@@ -1079,8 +1088,18 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
 int run_cg_tree_cluster(pins_workspace *ws, long long m, long long n, double mu, const double *rhs, double *x,
                         double rtol, int maxit, const double *gradf, const double *gradg, const double *a,
                         const double *b, cudaStream_t st) {
-    PINS_TRY(run_cg_tree(ws, m, n, mu, rhs, x, rtol, maxit, gradf, gradg, a, b, st, 1));
     const long long N = m + n;
+    // The preconditioner only has to be SPD: the factor of an earlier Newton system's
+    // M_T (an exact LDL^T of that SPD matrix) is one.  Late in EPPA the support and its
+    // weights change little between Newton systems, so while the PCG stays short the
+    // stored factor is reused instead of refactorised (the CG itself always multiplies
+    // by the current M, so the system solved and its residual test are unchanged).
+    static const int stale_its = getenv("PINS_STALE_ITS") ? atoi(getenv("PINS_STALE_ITS")) : 8;
+    static const int stale_max = getenv("PINS_STALE_MAX") ? atoi(getenv("PINS_STALE_MAX")) : 64;
+    const bool stale = ws->tree_valid && ws->tree_newton && ws->tree_N == N && ws->tree_last_its <= stale_its &&
+                       ws->tree_stale < stale_max;
+    if (stale) ++ws->tree_stale;
+    else PINS_TRY(run_cg_tree(ws, m, n, mu, rhs, x, rtol, maxit, gradf, gradg, a, b, st, 1));
     TreeCLArgs A;
     memset(&A, 0, sizeof A);
     A.m = (int)m;
@@ -1389,9 +1408,9 @@ int newton_iter(pins_workspace *ws, const pins_problem *pb, const pins_params *p
         acc[7] += hs[11];
         ++calls;
         if (calls % 200 == 1 || getenv("PINS_TREE_STATS")[0] == '2')
-            fprintf(stderr, "  last call: its %.0f rebuilt %.0f | kcycles mst %.1f fac %.1f pc %.1f (fwd %.1f warp %.1f bwd %.1f, R0/RW %.0f) mv %.1f total %.1f\n",
-                    cg_its, hs[11], hs[6] / 1e3, hs[7] / 1e3, hs[8] / 1e3, hs[12] / 1e3, hs[13] / 1e3, hs[14] / 1e3,
-                    hs[15], hs[9] / 1e3, hs[10] / 1e3);
+            fprintf(stderr, "  last call: its %.0f rebuilt %.0f stale %d rounds %.0f | kcycles mst %.1f fac %.1f pc %.1f (fwd %.1f warp %.1f bwd %.1f, R0/RW %.0f) mv %.1f total %.1f\n",
+                    cg_its, hs[11], ws->tree_stale, hs[4], hs[6] / 1e3, hs[7] / 1e3, hs[8] / 1e3, hs[12] / 1e3,
+                    hs[13] / 1e3, hs[14] / 1e3, hs[15], hs[9] / 1e3, hs[10] / 1e3);
         if (calls % 200 == 1)
             fprintf(stderr, "tree-cg calls %ld nnz %lld its %.0f rebuilds %.0f | Mcycles mst %.1f fac %.1f pc %.1f mv %.1f total %.1f\n",
                     calls, ws->nnz, cg_its, acc[7], acc[2] / 1e6, acc[3] / 1e6, acc[4] / 1e6, acc[5] / 1e6, acc[6] / 1e6);

@@ -121,6 +121,7 @@ struct PassSide {
     int skipk;                      // 0 off, 1 on
     int cps;                        // chunks per split (upper bound)
     float *gam;                     // [RB * S * cps * 4]: certificate per (row block, split, chunk, warp)
+    float *gamD;                    // [RB * S * cps * 4]: min distance Df over the same (warp rows, chunk)
     float *tref;                    // [M]: reference-pass row thresholds
     float *qref;                    // [N]: reference-pass skip-test column values
     int *skst;                      // [0] age (< 0: next pass records), [1] skipped, [2] chunks,
@@ -238,11 +239,14 @@ constexpr int kNBuf = COST == PC_DENSE_ROW ? 1 : 2;   // (the TMA ring stages de
 // integer points Df_ij is exact and the same in every pass.  A reference pass
 // records, per (row block, split, chunk), gamma >= max_i (max_j v_ij + |v| 2^-22
 // - T_i) with v the fp32 test values, T_i = the row's threshold then, and qref_j =
-// the column values then.  In a later pass with w_lo >= w_lo(ref),
-//     qs_j - w_lo Df_ij <= v_ij(real) + (qs_j - qref_j) <= gamma + T_i + max_j (qs_j - qref_j),
-// so if  gamma + max_j (qs_j - qref_j) <= min_i (thr32_i - T_i)  no entry of the
-// chunk can pass and the chunk is skipped: results are bit-identical with and
-// without skipping.  The potentials drift slowly between passes, so certificates
+// the column values then, and Dmin = min Df_ij over the same tile.  In a later
+// pass with w_lo >= w_lo(ref), dw = w_lo - w_lo(ref) >= 0,
+//     qs_j - w_lo Df_ij = v_ij(real) + (qs_j - qref_j) - dw Df_ij
+//                      <= gamma + T_i + max_j (qs_j - qref_j) - dw Dmin,
+// so if  gamma - dw Dmin + max_j (qs_j - qref_j) <= min_i (thr32_i - T_i)  no entry
+// of the chunk can pass and the chunk is skipped: results are bit-identical with
+// and without skipping.  (The dw Dmin term matters across EPPA iterations: w grows
+// with s_k, and the column values drift up by about as much as w D grows.)  The potentials drift slowly between passes, so certificates
 // stay valid for many passes; a pass records fresh ones when the skip fraction
 // falls (skip_switch).
 struct SkipCtx {
@@ -250,6 +254,8 @@ struct SkipCtx {
     double dthr;                // kind 1: min over the CTA's rows of thr32_i - T_i (rounded down)
     long long jb;               // the CTA's first column
     float *gcta;                // the CTA's certificates [cps * 4]
+    float *gDcta;               // the CTA's tile minimum distances [cps * 4]
+    double dw;                  // kind 1: w_lo - w_lo(reference) >= 0
     float *qref;
     bool wq;                    // kind 2: this CTA writes qref (row block 0)
 };
@@ -501,9 +507,18 @@ __device__ __forceinline__ int precheck_chunks(const PassSide &P, const SkipCtx 
         for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
         if (lane == 0) {
             const float4 g4 = __ldg(reinterpret_cast<const float4 *>(sk.gcta + c * 4));
-            const double g = (double)fmaxf(fmaxf(g4.x, g4.y), fmaxf(g4.z, g4.w));
+            const float4 d4 = __ldg(reinterpret_cast<const float4 *>(sk.gDcta + c * 4));
+            const float gv[4] = {g4.x, g4.y, g4.z, g4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+            double g = -INFINITY, gmag = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {        // per warp tile: gamma - dw Dmin
+                if (gv[q] == -INFINITY) continue;
+                const double t = (double)gv[q] - sk.dw * (double)dv[q];
+                g = fmax(g, t);
+                gmag = fmax(gmag, fabs((double)gv[q]) + sk.dw * (double)dv[q]);
+            }
             const double lhs = g + d - sk.dthr;
-            if (lhs + 1e-12 * (fabs(g) + fabs(d) + fabs(sk.dthr)) <= 0.0) atomicOr(bm + (c >> 5), 1u << (c & 31));
+            if (lhs + 1e-12 * (gmag + fabs(d) + fabs(sk.dthr)) <= 0.0) atomicOr(bm + (c >> 5), 1u << (c & 31));
         }
     }
     __syncthreads();
@@ -767,15 +782,17 @@ __device__ __forceinline__ double block_reduce_max(double v, double *sh) {
 // threads).  thr32 = the row's threshold at the start of the pass.
 __device__ __forceinline__ SkipCtx skip_setup(const PassSide &P, int rb, int sp, long long i, bool valid,
                                               long long jb, float thr32, float w_lo, double *red) {
-    SkipCtx sk{0, -INFINITY, jb, nullptr, P.qref, rb == 0};
+    SkipCtx sk{0, -INFINITY, jb, nullptr, nullptr, 0.0, P.qref, rb == 0};
     if (!P.skipk || P.skst[5] > 0) return sk;
     sk.gcta = P.gam + ((long long)rb * P.S + sp) * P.cps * 4;
+    sk.gDcta = P.gamD + ((long long)rb * P.S + sp) * P.cps * 4;
     if (skip_is_ref(P, w_lo)) {
         sk.kind = 2;
         if (valid && sp == 0) P.tref[i] = thr32;
         return sk;
     }
     sk.kind = 1;
+    sk.dw = (double)w_lo - (double)__int_as_float(P.skst[3]);     // exact; >= 0 (skip_is_ref)
     double d = INFINITY;
     if (valid) {
         const float t = P.tref[i];
@@ -788,12 +805,23 @@ __device__ __forceinline__ SkipCtx skip_setup(const PassSide &P, int rb, int sp,
 }
 
 // reference pass: certificate of this chunk for the warp's rows (all 32 lanes)
-__device__ __forceinline__ void record_cert(const SkipCtx &sk, long long j0, float vmx, float T, bool valid) {
+// dmn: the row's minimum Df over the chunk (any lower bound is valid; columns past
+// the end of a partial chunk may only lower it)
+__device__ __forceinline__ void record_cert(const SkipCtx &sk, long long j0, float vmx, float T, bool valid,
+                                            float dmn) {
     double e = -INFINITY;
     if (valid && vmx != -INFINITY) e = (double)vmx + fabs((double)vmx) * 0x1p-22 - (double)T;
+    float dm = valid ? fmaxf(dmn, 0.f) : INFINITY;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
-    if ((threadIdx.x & 31) == 0) sk.gcta[((j0 - sk.jb) / kCC) * 4 + (threadIdx.x >> 5)] = __double2float_ru(e);
+    for (int o = 16; o > 0; o >>= 1) {
+        e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+        dm = fminf(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        const long long k = ((j0 - sk.jb) / kCC) * 4 + (threadIdx.x >> 5);
+        sk.gcta[k] = __double2float_ru(e);
+        sk.gDcta[k] = dm == INFINITY ? 0.f : dm;
+    }
 }
 
 // phase 1 of a chunk (branch-free): the survivor mask of the fp32 test
@@ -803,11 +831,13 @@ __device__ __forceinline__ void record_cert(const SkipCtx &sk, long long j0, flo
 template <int COST>
 constexpr bool kDv = COST == PC_SQTC || COST == PC_SQ32 || COST == PC_L132;
 
-template <int COST, int DP>
+// REF (reference passes of the chunk skip only): also the row's maximum test value
+// vmx and minimum distance dmn over the chunk
+template <int COST, int DP, bool REF>
 __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSide &P, const RowPt<COST, DP> &rp,
                                            long long i, long long j0, int nc, const float *dots, float w_lo,
                                            float thr32, float (&Dv)[kDv<COST> ? kCC : 1], float &vmx,
-                                           const unsigned char *tile) {
+                                           float &dmn, const unsigned char *tile) {
     unsigned mask = 0u;
 #pragma unroll
     for (int c4 = 0; c4 < kCC; c4 += 4) {
@@ -832,7 +862,10 @@ __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSid
             const float v = fmaf(-w_lo, Df, qsv[j]);
             // columns c >= nc of a partial chunk are staged with q = -inf, so v = -inf there:
             // no per-entry range test is needed
-            vmx = fmaxf(vmx, v);
+            if constexpr (REF) {
+                vmx = fmaxf(vmx, v);
+                dmn = fminf(dmn, Df);
+            }
             mask |= (v > thr32) ? (1u << c) : 0u;
         }
     }
@@ -890,11 +923,13 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
         // phase 1: skip test against the chunk-start bound of the row max
         const float thr32 = thr_lo_of(mx - kLseCut);
         unsigned mask = 0u;
-        float vmx = -INFINITY;
+        float vmx = -INFINITY, dmn = INFINITY;
         float Dv[kDv<COST> ? kCC : 1];
-        if (valid)
-            mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, tile);
-        if (sk.kind == 2) record_cert(sk, j0, vmx, thr0, valid);
+        if (valid) {
+            if (sk.kind == 2) mask = phase1<COST, DP, true>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, dmn, tile);
+            else mask = phase1<COST, DP, false>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, dmn, tile);
+        }
+        if (sk.kind == 2) record_cert(sk, j0, vmx, thr0, valid, dmn);
         nsurv += __popc(mask);
         if constexpr (kDv<COST>) {
             // distances are needed only where some lane of the warp has a survivor
@@ -1038,11 +1073,13 @@ __device__ __forceinline__ void sum_side(const PassArgs &A, const PassSide &P, i
                              [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots,
                                  const unsigned char *tile) {
         unsigned mask = 0u;
-        float vmx = -INFINITY;
+        float vmx = -INFINITY, dmn = INFINITY;
         float Dv[kDv<COST> ? kCC : 1];
-        if (valid)
-            mask = phase1<COST, DP>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, tile);
-        if (sk.kind == 2) record_cert(sk, j0, vmx, thr32, valid);
+        if (valid) {
+            if (sk.kind == 2) mask = phase1<COST, DP, true>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, dmn, tile);
+            else mask = phase1<COST, DP, false>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, dmn, tile);
+        }
+        if (sk.kind == 2) record_cert(sk, j0, vmx, thr32, valid, dmn);
         nsurv += __popc(mask);
         if (!valid) return;
         if constexpr (COST == PC_SQTC) {

@@ -164,7 +164,10 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
         vs[h.x] = acc;
     };
     // M_T^-1 in place on vs (CTA 0 only)
+    long long t_fwd = 0, t_warp = 0, t_bwd = 0;
+    const long long t_start = clock64();
     auto tree_apply = [&]() {
+        const long long c0 = clock64();
         for (int rr = 0; rr < RW; ++rr) {
             const int q0r = rs[rr], q1 = rs[rr + 1];
             if (rr < R0) {
@@ -178,6 +181,7 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
             }
             __syncthreads();
         }
+        const long long c1 = clock64();
         if (warp == 0) {
             for (int rr = RW; rr < nrounds; ++rr) {
                 const int q = rs[rr] + lane;
@@ -199,6 +203,7 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
             }
         }
         __syncthreads();
+        const long long c2 = clock64();
         for (int rr = RW - 1; rr >= 0; --rr) {
             const int q0r = rs[rr], q1 = rs[rr + 1];
             if (rr < R0) {
@@ -220,6 +225,9 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
             }
             __syncthreads();
         }
+        t_fwd += c1 - c0;
+        t_warp += c2 - c1;
+        t_bwd += clock64() - c2;
     };
 
     // ---- init: x = x0, r = b - M x0, z = M_T^-1 r, p = z ----
@@ -371,6 +379,14 @@ __global__ void __cluster_dims__(kCGC, 1, 1) __launch_bounds__(kCGT, 1) cg_tree_
         A.st[1] = relres;
         A.st[2] = o2[0];
         A.st[3] = o2[1];
+        // dev instrumentation (PINS_TREE_STATS): rounds, CTA 0's cycles in the tree solve
+        A.st[4] = (double)nrounds;
+        A.st[8] = (double)(t_fwd + t_warp + t_bwd);
+        A.st[10] = (double)(clock64() - t_start);
+        A.st[12] = (double)t_fwd;
+        A.st[13] = (double)t_warp;
+        A.st[14] = (double)t_bwd;
+        A.st[15] = (double)(R0 * 1000 + RW);
     }
     cl.sync();   // keep shared memory alive until every remote access is done
 }
