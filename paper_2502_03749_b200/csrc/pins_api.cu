@@ -134,6 +134,8 @@ namespace {
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
+    unsigned gen = 0;      // bumped on every (re)allocation: the new memory holds no prior content
+                           // (cudaMalloc may hand back the same address, so pointers cannot tell)
     DevBuf() = default;
     DevBuf(const DevBuf &) = delete;
     DevBuf &operator=(const DevBuf &) = delete;
@@ -154,6 +156,20 @@ int ensure(DevBuf &b, size_t bytes) {
         return PINS_ERR_NOMEM;
     }
     b.bytes = bytes;
+    ++b.gen;
+    static long long n_alloc = 0;
+    const long long idx = n_alloc++;
+    static const long long plo = getenv("PINS_POISON_LO") ? atoll(getenv("PINS_POISON_LO")) : 0;
+    static const long long phi_ = getenv("PINS_POISON_HI") ? atoll(getenv("PINS_POISON_HI")) : (1LL << 60);
+    if (getenv("PINS_POISON_LIST") && idx >= plo && idx < phi_)
+        fprintf(stderr, "alloc %lld: %zu bytes\n", idx, bytes);
+    const char *pz = getenv("PINS_POISON");         // dev check: new buffers start as garbage
+    if (pz && idx >= plo && idx < phi_)
+    {
+        cudaDeviceSynchronize();
+        cudaMemset(b.p, atoi(pz) & 0xff, bytes);
+        cudaDeviceSynchronize();
+    }
     return PINS_OK;
 }
 
@@ -164,6 +180,8 @@ T *ptr(DevBuf &b) { return reinterpret_cast<T *>(b.p); }
 
 struct SideBufs {
     DevBuf pa, pb, pj, psc, blk, blkoff, ticket, cnt, bcol, bval, jstar;
+    // certified candidate lists of the Sinkhorn phase (pins_pass.cuh lse_sparse_kernel)
+    DevBuf lcnt, lj, lD, lB, lqref, lqv, lqsv, ldqc, ldqs, lperm, lq;
 };
 
 struct pins_workspace {
@@ -183,6 +201,9 @@ struct pins_workspace {
     CUtensorMap tm_row, tm_col;        // dense C staged by TMA (PC_DENSE_*_T)
     int S[2] = {1, 1};
     long long pcap = 16;       // per (row, split) sparsify capacity
+    long long lcap = 0;        // per (row, split) candidate-list capacity (0: not sized yet)
+    DevBuf lctl;               // candidate-list control ints
+    long long lstat[4] = {0, 0, 0, 0};   // dev statistics: record passes, sparse passes, overflows, fallbacks
     long long m = 0, n = 0, nnz = 0;
     int nsm = 0, dev = -1;
     bool tree_valid = false;
@@ -657,8 +678,70 @@ void base_args(pins_workspace *ws, const pins_problem *pb, double s, PassArgs &A
 }
 
 // One Sinkhorn half-sweep: o = 0 updates f (Alg. 2 line 5), o = 1 updates g (line 6).
+// the sparse path of a half-sweep: list walk, dense fallback of failed units, merge
+cudaError_t launch_lse_sparse(int cost, int dp, int grid, int gfb, int gmerge, size_t smem, cudaStream_t st,
+                              const PassArgs &A) {
+#define LSP_LAUNCH(C_, DP_)                                                                     \
+    do {                                                                                        \
+        if (smem)                                                                               \
+            LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_sparse_kernel<C_, DP_, true><<<grid, kPT,       \
+                   pass_smem(lse_sparse_kernel<C_, DP_, true>, 64 * 1024 + 16) ? smem : 0, st>>>(A)); \
+        else                                                                                    \
+            LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_sparse_kernel<C_, DP_, false><<<grid, kPT, 0, st>>>(A)); \
+        LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_fallback_kernel<C_, DP_><<<gfb, kPT, 0, st>>>(A));  \
+        LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_merge_kernel<<<gmerge, kPT, 0, st>>>(A));           \
+    } while (0)
+    switch (cost) {
+        case PC_DENSE_ROW: case PC_DENSE_ROW_T: LSP_LAUNCH(PC_DENSE_ROW_T, 4); break;
+        case PC_DENSE_COL: case PC_DENSE_COL_T: LSP_LAUNCH(PC_DENSE_COL_T, 4); break;
+        case PC_SQ32: PINS_DP_DISPATCH(dp, LSP_LAUNCH(PC_SQ32, DP)); break;
+        case PC_L132: PINS_DP_DISPATCH(dp, LSP_LAUNCH(PC_L132, DP)); break;
+        case PC_SQ64: PINS_DP_DISPATCH(dp, LSP_LAUNCH(PC_SQ64, DP)); break;
+        case PC_SQTC: PINS_DP_DISPATCH(dp, LSP_LAUNCH(PC_SQTC, DP)); break;
+        default: PINS_DP_DISPATCH(dp, LSP_LAUNCH(PC_L164, DP)); break;
+    }
+#undef LSP_LAUNCH
+    return cudaGetLastError();
+}
+
+// candidate-list margin below the LSE cut (units of the exponent): wider lists, fewer
+// record passes
+double list_margin() {
+    const char *e = getenv("PINS_LIST_MARGIN");
+    return e ? atof(e) : 4.0;
+}
+
+// candidate-list buffers of both sides at capacity ws->lcap per (row, split)
+int ensure_lists(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
+    for (int o = 0; o < 2; ++o) {
+        const long long M = o == 0 ? pb->m : pb->n, N = o == 0 ? pb->n : pb->m, S = ws->S[o];
+        const int cost = o == 0 ? ws->cost_row : ws->cost_col;
+        const size_t dsz = (cost == PC_SQTC || cost == PC_SQ32 || cost == PC_L132) ? 4 : 8;
+        SideBufs &B = ws->sb[o];
+        PINS_TRY(ensure(B.lcnt, sizeof(int) * S * M));
+        PINS_TRY(ensure(B.lj, sizeof(int) * S * ws->lcap * M));
+        PINS_TRY(ensure(B.lD, dsz * S * ws->lcap * M));
+        PINS_TRY(ensure(B.lB, sizeof(float) * M));
+        PINS_TRY(ensure(B.lqref, sizeof(float) * N));
+        PINS_TRY(ensure(B.lqv, sizeof(double) * N));
+        PINS_TRY(ensure(B.lqsv, sizeof(float) * N));
+        PINS_TRY(ensure(B.ldqc, sizeof(float) * (N / kCC + 2)));
+        PINS_TRY(ensure(B.ldqs, sizeof(float) * S));
+        PINS_TRY(ensure(B.lperm, sizeof(int) * S * M));
+        PINS_TRY(ensure(B.lq, sizeof(int) * S * M));
+    }
+    PINS_TRY(ensure(ws->lctl, sizeof(int) * 16));
+    (void)st;
+    return PINS_OK;
+}
+
+// One Sinkhorn half-sweep: o = 0 updates f (Alg. 2 line 5), o = 1 updates g (line 6).
+// lmode 0: the dense pass alone; 1: the dense pass if the side's candidate lists must
+// be recorded (it records them), then the sparse pass over the lists otherwise (lt:
+// this half-sweep's launch index).
 int half_sweep(pins_workspace *ws, const pins_problem *pb, int o, const double *phi, const double *psi,
-               double s, double *f, double *g, bool check_done, bool test_tol, cudaStream_t st) {
+               double s, double *f, double *g, bool check_done, bool test_tol, cudaStream_t st,
+               int lmode = 0, int lt = 0) {
     PassArgs A;
     base_args(ws, pb, s, A);
     fill_side(ws, pb, o, f, phi, g, psi, A.side[0]);
@@ -672,6 +755,42 @@ int half_sweep(pins_workspace *ws, const pins_problem *pb, int o, const double *
     A.test_tol = test_tol ? 1 : 0;
     A.sink_tol = ptr<double>(ws->tol);
     const int cost = o == 0 ? ws->cost_row : ws->cost_col;
+    if (lmode) {
+        PassSide &P = A.side[0];
+        SideBufs &B = ws->sb[o], &Bo = ws->sb[1 - o];
+        P.lori = o;
+        P.lcap = (int)ws->lcap;
+        P.lcnt = ptr<int>(B.lcnt);
+        P.lj = ptr<int>(B.lj);
+        P.lD = B.lD.p;
+        P.lB = ptr<float>(B.lB);
+        P.lqref = ptr<float>(B.lqref);
+        P.lqv = ptr<double>(B.lqv);
+        P.lqsv = ptr<float>(B.lqsv);
+        P.ldqs = ptr<float>(B.ldqs);
+        P.lperm = ptr<int>(B.lperm);
+        P.lq = ptr<int>(B.lq);
+        P.oqv = ptr<double>(Bo.lqv);
+        P.oqsv = ptr<float>(Bo.lqsv);
+        P.oqref = ptr<float>(Bo.lqref);
+        P.odqc = ptr<float>(Bo.ldqc);
+        P.odqs = ptr<float>(Bo.ldqs);
+        P.oS = ws->S[1 - o];
+        P.lctl = ptr<int>(ws->lctl);
+        A.lt = lt;
+        A.lmargin = list_margin();
+        P.lrec = 1;
+        PINS_CUDA(launch_lse(cost, ws->dp, A.G0, st, A, o == 0 ? ws->tm_row : ws->tm_col));
+        P.lrec = 0;
+        LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_sort_kernel<<<P.S, 1024, 0, st>>>(A));
+        // the widest split's column values (q fp64 + qs fp32) staged per CTA when they fit
+        const long long nch = (P.N + kCC - 1) / kCC, wmax = kCC * ((nch + P.S - 1) / P.S);
+        const size_t stage = (size_t)wmax * 12 + 16;
+        P.lstage = stage <= 64 * 1024 ? 1 : 0;
+        PINS_CUDA(launch_lse_sparse(cost, ws->dp, (int)(P.S * ((P.M + kPT - 1) / kPT)), 4 * ws->nsm, P.RB,
+                                    P.lstage ? stage : 0, st, A));
+        return PINS_OK;
+    }
     PINS_CUDA(launch_lse(cost, ws->dp, A.G0, st, A, o == 0 ? ws->tm_row : ws->tm_col));
     return PINS_OK;
 }
@@ -702,17 +821,28 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
     double tolv = prm->sink_tol;
     PINS_CUDA(cudaMemcpyAsync(ws->tol.p, &tolv, sizeof(double), cudaMemcpyHostToDevice, st));
     PINS_CUDA(cudaMemsetAsync(ws->ctl.p, 0, sizeof(int) * 8, st));
-    int done = 0, batch = 1, queued = 0;
+    // certified candidate lists (lse_sparse_kernel): recorded by the first sweep of the
+    // phase and again whenever a certificate fails; bit-identical to the dense sweeps
+    const bool lists = getenv("PINS_SPARSE_SWEEP") != nullptr && prm->T1 > 1;
+    if (lists) {
+        if (ws->lcap == 0) ws->lcap = getenv("PINS_LIST_CAP") ? std::max(1LL, atoll(getenv("PINS_LIST_CAP"))) : 64;
+        ws->lcap = (ws->lcap + 7) / 8 * 8;        // lists padded to whole batches of 8
+        PINS_TRY(ensure_lists(ws, pb, st));
+        const int init[16] = {1, 1, -1, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        PINS_CUDA(cudaMemcpyAsync(ws->lctl.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+    }
+    int done = 0, batch = 1, queued = 0, lt = 0;
+    int *hc = reinterpret_cast<int *>(ws->h + 40);
     while (!done && queued < prm->T1) {
         const int nb = std::min(batch, prm->T1 - queued);
         for (int q = 0; q < nb; ++q) {
             const bool first = (queued + q) == 0;
-            PINS_TRY(half_sweep(ws, pb, 0, phi, psi, s, f, g, true, !first, st));
-            PINS_TRY(half_sweep(ws, pb, 1, phi, psi, s, f, g, true, false, st));
+            PINS_TRY(half_sweep(ws, pb, 0, phi, psi, s, f, g, true, !first, st, lists ? 1 : 0, lt++));
+            PINS_TRY(half_sweep(ws, pb, 1, phi, psi, s, f, g, true, false, st, lists ? 1 : 0, lt++));
         }
         queued += nb;
-        int *hc = reinterpret_cast<int *>(ws->h + 40);
         PINS_CUDA(cudaMemcpyAsync(hc, ws->ctl.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+        if (lists) PINS_CUDA(cudaMemcpyAsync(hc + 4, ws->lctl.p, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
         PINS_CUDA(cudaStreamSynchronize(st));
         done = hc[0];
         *sweeps_out = hc[1];
@@ -720,6 +850,22 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
             PINS_CUDA(cudaMemcpyAsync(f, ws->fsave.p, sizeof(double) * pb->m, cudaMemcpyDeviceToDevice, st));
         }
         batch = std::min(batch * 2, 64);
+        if (lists && !done && hc[4 + 4] > 0) {
+            // a list past capacity (its (split, row) scans densely): grow the lists (the
+            // stream is idle here) and record them again
+            ws->lcap = (std::max<long long>(2 * ws->lcap, (long long)(1.25 * hc[4 + 5]) + 8) + 7) / 8 * 8;
+            PINS_TRY(ensure_lists(ws, pb, st));
+            const int init[14] = {1, 1, -1, -1, 0, 0, hc[4 + 6], hc[4 + 7], 0, 0, 0, 0, hc[4 + 12], hc[4 + 13]};
+            PINS_CUDA(cudaMemcpyAsync(ws->lctl.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+            ++ws->lstat[2];
+        }
+    }
+    if (lists) {
+        ws->lstat[3] += hc[4 + 6] + hc[4 + 7];
+        if (getenv("PINS_LIST_STATS"))     // dev instrumentation
+            fprintf(stderr, "lists: sweeps %d cap %lld max %d overflow %d fallback units %d / %d records %d / %d "
+                    "entries recorded %d / %d\n", hc[1], ws->lcap, hc[4 + 5], hc[4 + 4], hc[4 + 6], hc[4 + 7],
+                    hc[4 + 12], hc[4 + 13], hc[4 + 14], hc[4 + 15]);
     }
     return PINS_OK;
 }
@@ -984,12 +1130,12 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     const long long ni_fixed = 15 * N + 1 + kTreeMaxRounds + 1 + 8 + (11 * N + 1);   // + pull lists
     const long long ni = ni_fixed + nnz;
     const long long nd = 4 * N + 2 * N + N + 3 * N + 4 * N + 3 * N + 5 * N;   // pull entries, tw, dcur, fc1/fc2/finv, r z p q, tval fw1 fw2, frec
-    const void *old_i = ws->tr_i.p, *old_d = ws->tr_d.p;
+    const unsigned old_i = ws->tr_i.gen, old_d = ws->tr_d.gen;
     PINS_TRY(ensure(ws->tr_i, sizeof(int) * ni));
     PINS_TRY(ensure(ws->tr_d, sizeof(double) * nd));
     PINS_TRY(ensure(ws->tr_u8, (size_t)(nnz + 2 * N)));
     PINS_TRY(ensure(ws->tr_u64, sizeof(unsigned long long) * N));
-    if (ws->tr_i.p != old_i || ws->tr_d.p != old_d || ws->tree_N != N) ws->tree_valid = false;
+    if (ws->tr_i.gen != old_i || ws->tr_d.gen != old_d || ws->tree_N != N) ws->tree_valid = false;
     TreeArgs A;
     memset(&A, 0, sizeof A);
     A.m = (int)m;
@@ -1058,7 +1204,7 @@ int run_cg_tree(pins_workspace *ws, long long m, long long n, double mu, const d
     A.best = ptr<unsigned long long>(ws->tr_u64);
     // reuse the stored tree while it keeps CG short (the kernel also checks that
     // every tree edge is still in the support and rebuilds otherwise)
-    A.reuse = ws->tree_valid && ws->tree_last_its <= 48 && !force_rebuild ? 1 : 0;
+    A.reuse = ws->tree_valid && ws->tree_last_its <= 48 && !force_rebuild && !getenv("PINS_TREE_NO_REUSE") ? 1 : 0;
     A.setup_only = setup_only;
     ws->tree_rstart = A.rstart;
     ws->tree_ctr = A.ctr;

@@ -152,6 +152,34 @@ struct PassSide {
     double *blk;                    // [RB * 8] per row block scalars
     long long *blkoff;              // SUM: [RB + 1] exclusive scan of the block nnz totals
     unsigned *ticket;               // [RB]
+    // Certified candidate lists of the Sinkhorn phase (LSE only; see lse_sparse_kernel).
+    // Unit u = sp * M + i is (split sp, pass row i); its list holds, in column order, the
+    // entries with test value v > lB[i] at the last record pass, unit-major at u * lcap.
+    int lori;                       // orientation (0 rows, 1 columns): index into lctl
+    int lrec;                       // dense pass: record the lists (conditional on lctl[lori])
+    int lcap;                       // capacity per unit
+    int *lcnt;                      // [S * M] entries per unit, -1 = overflow
+    int *lj;                        // [S * M * lcap] columns
+    void *lD;                       // [S * M * lcap] distances: float (exact-fp32 costs) or double
+    float *lB;                      // [M] the record pass's list bound lB_i = thr0_i - margin
+    float *lqref;                   // [N] the record pass's column test values qs_j
+    const double *lqv;              // [N] sparse pass: column values q_j (written by the other side)
+    const float *lqsv;              // [N] sparse pass: qs_of(q_j)
+    const float *ldqs;              // [S] sparse pass: per split max_j (qs_j - lqref_j) since the record
+    int *lperm;                     // [S * M] units by decreasing list length (after each record)
+    int *lq;                        // [S * M] units whose certificate failed (fallback queue)
+    int lstage;                     // sparse pass: the split's column values staged in shared memory
+    // finalize: this side's new potentials are the other side's column values
+    double *oqv;                    // [M] q of the other orientation, or NULL
+    float *oqsv;                    // [M]
+    const float *oqref;             // [M] the other side's lqref
+    float *odqc;                    // [M / kCC + 1] scratch: per chunk drift of the other side's columns
+    float *odqs;                    // [oS] the other side's ldqs
+    int oS;                         // the other side's splits
+    int *lctl;                      // [0..1] rebuild requested per side, [2..3] launch index of the
+                                    // last record per side, [4] overflows, [5] max count, [6..7]
+                                    // fallback units (stats), [8] fallback queue length, [12..13]
+                                    // record passes (stats)
 };
 
 struct PassArgs {
@@ -170,7 +198,13 @@ struct PassArgs {
     int count_sweep;                // LSE col pass: ++ctl[1]
     int test_tol;                   // LSE row pass: set done (and rollback) when res <= tol
     const double *a_dot, *f_dot, *b_dot, *g_dot;   // SUM: <a,f> + <b,g> (global finalize)
+    int lt;                         // candidate lists: launch index of this half-sweep
+    double lmargin;                 // candidate lists: record margin below the threshold
 };
+
+// candidate-list distance storage: the exact fp32 distance where phase 1 keeps one, else fp64
+template <int COST>
+using LDT = typename std::conditional<COST == PC_SQTC || COST == PC_SQ32 || COST == PC_L132, float, double>::type;
 
 // Column range of split sp of S: whole kCC-column chunks (so every chunk starts at
 // a multiple of kCC -- TMA box origins stay 256-byte aligned), the last split
@@ -199,6 +233,11 @@ __device__ __forceinline__ void count_survivors(int on, int slot, int nsurv) {
 // every fp32 rounding), so no entry the fp64 test keeps is skipped (R10).
 __device__ __forceinline__ float qs_of(double q) {
     return q == -INFINITY ? -INFINITY : (float)(q + fabs(q) * 0x1p-20);
+}
+// the spacing of floats at |x| (an upper bound of the rounding error of a value near x)
+__device__ __forceinline__ float ulpf_of(float x) {
+    const float a = fabsf(x);
+    return a == INFINITY ? INFINITY : nextafterf(a, INFINITY) - a;
 }
 __device__ __forceinline__ float thr_lo_of(double t) { return (float)(t - fabs(t) * 0x1p-20 - 0x1p-30); }
 
@@ -833,11 +872,12 @@ constexpr bool kDv = COST == PC_SQTC || COST == PC_SQ32 || COST == PC_L132;
 
 // REF (reference passes of the chunk skip only): also the row's maximum test value
 // vmx and minimum distance dmn over the chunk
-template <int COST, int DP, bool REF>
+template <int COST, int DP, bool REF, bool REC = false>
 __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSide &P, const RowPt<COST, DP> &rp,
                                            long long i, long long j0, int nc, const float *dots, float w_lo,
                                            float thr32, float (&Dv)[kDv<COST> ? kCC : 1], float &vmx,
-                                           float &dmn, const unsigned char *tile) {
+                                           float &dmn, const unsigned char *tile, float lb = 0.f,
+                                           unsigned *rmask = nullptr) {
     unsigned mask = 0u;
 #pragma unroll
     for (int c4 = 0; c4 < kCC; c4 += 4) {
@@ -866,6 +906,7 @@ __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSid
                 vmx = fmaxf(vmx, v);
                 dmn = fminf(dmn, Df);
             }
+            if constexpr (REC) *rmask |= (v > lb) ? (1u << c) : 0u;
             mask |= (v > thr32) ? (1u << c) : 0u;
         }
     }
@@ -877,6 +918,117 @@ __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSid
 // Stats written by the global finalizer: st[0] = residual ||a - X~ e||_1 of
 // the starting iterate (pass-row side), st[1] = max |f_new - f_old|.
 // =========================================================================
+// Row-block and launch finalize of a half-sweep (the dense kernel after its split
+// ticket, the sparse path's merge kernel directly): merge the S split partials of
+// each pass row in split order, update the potential, residual of the starting
+// iterate, argmax seed; for the candidate lists the new potentials become the other
+// side's column values, with their drift since that side's record pass.
+__device__ __forceinline__ void lse_rowblock_finalize(const PassArgs &A, const PassSide &P, int rb, long long i,
+                                                      bool valid, const double *thi, const double *tlo, double *red,
+                                                      bool *flag, float w_lo, bool rec_ran, bool sparse) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const double inv_eta = A.inv_eta;
+    double res = 0.0, dmax = 0.0, dq = -INFINITY;
+    if (valid) {
+        // split partials in batches of 8 (independent loads first; the max and the sum
+        // then run in split order, as before)
+        double M = -INFINITY;
+        int jbest = -1;
+        for (int s0 = 0; s0 < P.S; s0 += 8) {
+            double v[8];
+            int jj[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int s = min(s0 + q, P.S - 1);
+                v[q] = P.pa[(long long)s * P.M + i];
+                jj[q] = P.pj[(long long)s * P.M + i];
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (s0 + q < P.S && v[q] > M) { M = v[q]; jbest = jj[q]; }
+        }
+        double Ssum = 0.0;
+        for (int s0 = 0; s0 < P.S; s0 += 8) {
+            double v[8], c[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int s = min(s0 + q, P.S - 1);
+                v[q] = P.pa[(long long)s * P.M + i];
+                c[q] = P.pb[(long long)s * P.M + i];
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (s0 + q < P.S && c[q] > 0.0) Ssum += c[q] * pexp(v[q] - M, thi, tlo);
+        }
+        const double L = M + log(Ssum);
+        const double fo = P.fr[i], ph = P.phir[i], a = P.ar[i];
+        // residual of the starting iterate: row sum = exp(P_i + L)
+        const double r = exp(pot_p(fo, ph, inv_eta) + L);
+        res = fabs(a - r);
+        const double fn = A.eta * (log(a) + 1.0 - L) - ph;
+        dmax = fabs(fn - fo);
+        if (P.fsave) P.fsave[i] = fo;
+        P.fout[i] = fn;
+        if (jbest >= 0) P.jstar[i] = jbest;
+        if (P.oqv) {                          // the other orientation's column value of this row
+            const double q = pot_q(fn, ph, inv_eta);
+            const float qs = qs_of(q);
+            P.oqv[i] = q;
+            P.oqsv[i] = qs;
+            dq = qs == -INFINITY ? -INFINITY : (double)qs - (double)P.oqref[i];
+        }
+    }
+    if (P.oqv) {      // a warp's 32 pass rows are one chunk of the other side's columns
+        const double wq = warp_max(dq);
+        if (lane == 0 && i < P.M) P.odqc[i >> 5] = wq == -INFINITY ? -INFINITY : __double2float_ru(wq);
+    }
+    const double bres = block_reduce_sum(res, red);
+    const double bdm = block_reduce_max(dmax, red);
+    if (tid == 0) {
+        P.blk[rb * 8 + 0] = bres;
+        P.blk[rb * 8 + 1] = bdm;
+    }
+    if (!last_arrival(A.gticket, (unsigned)P.RB, flag)) return;
+    // ---- launch finalize ----
+    double v0 = 0.0, v1 = 0.0;
+    for (int b = tid; b < P.RB; b += kPT) {     // deterministic: fixed assignment + fixed tree
+        v0 += P.blk[b * 8 + 0];
+        v1 = fmax(v1, P.blk[b * 8 + 1]);
+    }
+    const double R = block_reduce_sum(v0, red);
+    const double DM = block_reduce_max(v1, red);
+    if (P.oqv) {      // per split of the other side: the largest chunk drift of its columns
+        for (int sp = tid; sp < P.oS; sp += kPT) {
+            long long jb, je;
+            split_range(P.M, P.oS, sp, jb, je);
+            float mx = -INFINITY;
+            for (long long c = jb / kCC; c < (je + kCC - 1) / kCC; ++c) mx = fmaxf(mx, P.odqc[c]);
+            P.odqs[sp] = mx;
+        }
+    }
+    if (tid == 0) {
+        A.st[0] = R;
+        A.st[1] = DM;
+        if (A.count_sweep) A.ctl[1] += 1;
+        skip_switch(P, w_lo);
+        if (rec_ran) {                        // lists recorded: the sparse path of this half-sweep exits
+            P.lctl[P.lori] = 0;
+            P.lctl[2 + P.lori] = A.lt;
+            P.lctl[12 + P.lori] += 1;
+        }
+        if (sparse) {                         // record again once > 2 % of the units fell back
+            const long long U = (long long)P.S * P.M;
+            if (50LL * P.lctl[8] > U) P.lctl[P.lori] = 1;
+            P.lctl[6 + P.lori] += P.lctl[8];
+            P.lctl[8] = 0;
+        }
+        if (A.test_tol && A.sink_tol && R <= *A.sink_tol) {
+            A.ctl[0] = 1;     // converged at the starting iterate: roll back this update
+            A.ctl[2] = 1;
+        }
+    }
+}
+
 template <int COST, int DP>
 __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __grid_constant__ CUtensorMap tm0) {
     extern __shared__ __align__(1024) unsigned char dyn_smem[];   // TMA ring (dense costs) or unused
@@ -889,6 +1041,9 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
     __shared__ bool flag;
     if (A.check_done && A.ctl[0]) return;            // Sinkhorn phase already converged
     const PassSide &P = A.side[0];
+    // candidate lists: this dense pass runs only when the lists must be (re)recorded
+    const bool rec = P.lrec != 0;
+    if (rec && P.lctl[P.lori] == 0) return;
     const int tid = threadIdx.x;
     const int rb = blockIdx.x % P.RB, sp = blockIdx.x / P.RB;
     const long long i0 = (long long)rb * kPT, i = i0 + tid;
@@ -915,30 +1070,64 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
     float *dsc = dscr + tid * (kCC + 1);       // this thread's chunk distances (kDv costs)
     int nsurv = 0;
     const float thr0 = thr_lo_of(mx - kLseCut);
-    const SkipCtx sk = skip_setup(P, rb, sp, i, valid, jb, thr0, w_lo, red);
+    // record pass: every entry with v > lb goes to the list (lb = thr0 - margin); the
+    // chunk skip then certifies against lb, so skipped chunks hold no list entry either
+    const float lb = rec ? (mx == -INFINITY ? -INFINITY : __double2float_rd((double)thr0 - A.lmargin)) : thr0;
+    const long long lbase = ((long long)sp * P.M + i) * P.lcap;      // unit-major lists
+    int lk = 0;
+    if (rec && valid && sp == 0) P.lB[i] = lb;
+    if (rec && rb == 0)             // the record's column test values (also of chunks skipped below)
+        for (long long j = jb + tid; j < je; j += kPT) P.lqref[j] = qs_of(pot_q(P.gc[j], P.psic[j], inv_eta));
+    const SkipCtx sk = skip_setup(P, rb, sp, i, valid, jb, lb, w_lo, red);
     const TmaRing ring = ring_setup<COST>(dyn_smem, ring_full, &tm0, i0);
     const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, 0, false, bufs, &tcs, sk, ring,
                              [&](long long j0, int nc, const Buf<COST, DP> &B, const float *dots,
                                  const unsigned char *tile) {
         // phase 1: skip test against the chunk-start bound of the row max
         const float thr32 = thr_lo_of(mx - kLseCut);
-        unsigned mask = 0u;
+        unsigned mask = 0u, rmask = 0u;
         float vmx = -INFINITY, dmn = INFINITY;
         float Dv[kDv<COST> ? kCC : 1];
         if (valid) {
-            if (sk.kind == 2) mask = phase1<COST, DP, true>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, dmn, tile);
-            else mask = phase1<COST, DP, false>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, dmn, tile);
+            if (rec) {
+                if (sk.kind == 2)
+                    mask = phase1<COST, DP, true, true>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, dmn, tile,
+                                                        lb, &rmask);
+                else
+                    mask = phase1<COST, DP, false, true>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, dmn, tile,
+                                                         lb, &rmask);
+            } else if (sk.kind == 2) {
+                mask = phase1<COST, DP, true>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, dmn, tile);
+            } else {
+                mask = phase1<COST, DP, false>(B, P, rp, i, j0, nc, dots, w_lo, thr32, Dv, vmx, dmn, tile);
+            }
         }
-        if (sk.kind == 2) record_cert(sk, j0, vmx, thr0, valid, dmn);
+        if (sk.kind == 2) record_cert(sk, j0, vmx, lb, valid, dmn);
         nsurv += __popc(mask);
         if constexpr (kDv<COST>) {
             // distances are needed only where some lane of the warp has a survivor
-            if (__any_sync(0xffffffffu, mask != 0u)) {
+            if (__any_sync(0xffffffffu, (mask | rmask) != 0u)) {
 #pragma unroll
                 for (int c = 0; c < kCC; ++c) dsc[c] = Dv[c];
             }
         }
         if (!valid) return;
+        if (rec) {                                 // append this chunk's list entries
+            LDT<COST> *lD = reinterpret_cast<LDT<COST> *>(P.lD);
+            while (rmask) {
+                const int c = __ffs(rmask) - 1;
+                rmask &= rmask - 1u;
+                if (lk >= 0 && lk < P.lcap) {
+                    const long long e = lbase + lk;
+                    P.lj[e] = (int)(j0 + c);
+                    if constexpr (kDv<COST>) lD[e] = dsc[c];
+                    else lD[e] = (LDT<COST>)chunk_dist<COST, DP>(B, P, rp, i, j0, c, tile);
+                    ++lk;
+                } else {
+                    lk = -1;                       // overflow: this (split, row) falls back to dense
+                }
+            }
+        }
         // phase 2: the surviving entries of this row, two per iteration (independent
         // exponentials).  The reference mx is a true entry; sm accumulates exp(x - mx)
         // for x <= mx + 1 and a larger x (rare once the argmax seed is in place) becomes
@@ -972,59 +1161,354 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
         P.pa[(long long)sp * P.M + i] = mx;
         P.pb[(long long)sp * P.M + i] = sm;
         P.pj[(long long)sp * P.M + i] = jm;
+        if (rec) {
+            // pad the list to whole batches of 8 with entries that can never survive
+            // (distance +inf: test value -inf), so the walk loads whole batches
+            if (lk > 0 && (lk & 7)) {
+                LDT<COST> *lD = reinterpret_cast<LDT<COST> *>(P.lD);
+                const int jl = P.lj[lbase + lk - 1];
+                for (int k = lk; k < ((lk + 7) & ~7); ++k) {
+                    P.lj[lbase + k] = jl;
+                    lD[lbase + k] = (LDT<COST>)INFINITY;
+                }
+            }
+            P.lcnt[(long long)sp * P.M + i] = lk;
+            if (lk < 0) atomicAdd(P.lctl + 4, 1);
+            else {
+                atomicMax(P.lctl + 5, lk);
+                atomicAdd(P.lctl + 14 + P.lori, lk);      // entries of the last record (stats)
+            }
+        }
     }
     if (!last_arrival(P.ticket + rb, (unsigned)P.S, &flag)) return;
-    // ---- row-block finalize: merge the S splits (in split order) ----
-    double res = 0.0, dmax = 0.0;
-    if (valid) {
-        double M = -INFINITY;
-        int jbest = -1;
-        for (int s = 0; s < P.S; ++s) {
-            const double v = P.pa[(long long)s * P.M + i];
-            if (v > M) { M = v; jbest = P.pj[(long long)s * P.M + i]; }
-        }
-        double Ssum = 0.0;
-        for (int s = 0; s < P.S; ++s) {
-            const double v = P.pa[(long long)s * P.M + i];
-            const double c = P.pb[(long long)s * P.M + i];
-            if (c > 0.0) Ssum += c * pexp(v - M, thi, tlo);
-        }
-        const double L = M + log(Ssum);
-        const double fo = P.fr[i], ph = P.phir[i], a = P.ar[i];
-        // residual of the starting iterate: row sum = exp(P_i + L)
-        const double r = exp(pot_p(fo, ph, inv_eta) + L);
-        res = fabs(a - r);
-        const double fn = A.eta * (log(a) + 1.0 - L) - ph;
-        dmax = fabs(fn - fo);
-        if (P.fsave) P.fsave[i] = fo;
-        P.fout[i] = fn;
-        if (jbest >= 0) P.jstar[i] = jbest;
-    }
-    const double bres = block_reduce_sum(res, red);
-    const double bdm = block_reduce_max(dmax, red);
+    lse_rowblock_finalize(A, P, rb, i, valid, thi, tlo, red, &flag, w_lo, rec, false);
+}
+
+// =========================================================================
+// Sparse LSE half-sweep over the certified candidate lists (Sinkhorn phase).
+//
+// The record pass (lse_pass_kernel with lrec) lists, per unit (split sp, pass row i),
+// every entry with fp32 test value v > lB_i = thr0_i - margin, in column order.
+// Certificate of a unit in a later pass (same w: one Sinkhorn phase): an unlisted
+// entry had fl(qs_j - w_lo D_ij) <= lB_i, so its real value now is at most
+// lB_i + ulp(lB_i) + (qs_j(now) - qs_j(record)) <= lB_i + ulp + ldqs[sp].  If that is
+// <= thr0_i (this pass's starting threshold, below every chunk threshold of the dense
+// pass), no unlisted entry passes the dense pass's fp32 test, and walking the list
+// with the dense pass's chunk-start thresholds, survivor pairing and reference updates
+// gives bit-identical partials.  Units that fail go to a queue that
+// lse_fallback_kernel scans densely (one warp per unit, same arithmetic);
+// lse_merge_kernel then merges the split partials.  After each record, lse_sort_kernel
+// orders the units by decreasing list length, so the threads of a warp walk lists of
+// about the same length (no divergence) and the long ones start first.
+// =========================================================================
+// per split, the pass rows by decreasing list length (counting sort in 64 length
+// buckets, one CTA per split); only right after a record
+__global__ void __launch_bounds__(1024) lse_sort_kernel(PassArgs A) {
+    const PassSide &P = A.side[0];
+    if (P.lctl[2 + P.lori] != A.lt) return;
+    __shared__ int hist[64];
+    const int sp = blockIdx.x, tid = threadIdx.x;
+    const int *cnt = P.lcnt + (long long)sp * P.M;
+    int *perm = P.lperm + (long long)sp * P.M;
+    if (tid < 64) hist[tid] = 0;
+    __syncthreads();
+    auto key = [&](long long i) {
+        const int c = cnt[i];
+        return c < 0 ? 0 : 63 - min(63, c >> 3);           // descending length; overflow first
+    };
+    for (long long i = tid; i < P.M; i += 1024) atomicAdd(hist + key(i), 1);
+    __syncthreads();
     if (tid == 0) {
-        P.blk[rb * 8 + 0] = bres;
-        P.blk[rb * 8 + 1] = bdm;
+        int acc = 0;
+        for (int k = 0; k < 64; ++k) { const int h = hist[k]; hist[k] = acc; acc += h; }
     }
-    if (!last_arrival(A.gticket, (unsigned)P.RB, &flag)) return;
-    // ---- launch finalize ----
-    double v0 = 0.0, v1 = 0.0;
-    for (int b = tid; b < P.RB; b += kPT) {     // deterministic: fixed assignment + fixed tree
-        v0 += P.blk[b * 8 + 0];
-        v1 = fmax(v1, P.blk[b * 8 + 1]);
+    __syncthreads();
+    for (long long i = tid; i < P.M; i += 1024) perm[atomicAdd(hist + key(i), 1)] = (int)i;
+}
+
+template <int COST, int DP, bool STG>
+__global__ void __launch_bounds__(kPT) lse_sparse_kernel(PassArgs A) {
+    constexpr int kLB = 8;                           // list entries per batch
+    extern __shared__ __align__(16) unsigned char lsm[];   // the split's column values
+    __shared__ double thi[64], tlo[64];
+    __shared__ double sx[kLB * kPT], se[kLB * kPT];  // the batch, [entry][thread]
+    __shared__ int sj[kLB * kPT];
+    if (A.check_done && A.ctl[0]) return;            // Sinkhorn phase already converged
+    const PassSide &P = A.side[0];
+    if (P.lctl[2 + P.lori] == A.lt) return;          // the dense pass recorded this half-sweep
+    // CTA = 128 consecutive ranks (by list length) of one split; the longest groups of
+    // all splits come first (longest-first scheduling)
+    const int sp = blockIdx.x % P.S;
+    const long long t = (long long)(blockIdx.x / P.S) * kPT + threadIdx.x;
+    long long jb, je;
+    split_range(P.N, P.S, sp, jb, je);
+    load_exp_table(A.tab, thi, tlo);
+    // the split's column values in shared memory (STG: when they fit), else from global
+    double *sq = reinterpret_cast<double *>(lsm);
+    float *sqs = reinterpret_cast<float *>(sq + (STG ? je - jb : 0));
+    if constexpr (STG)
+        for (long long j = jb + threadIdx.x; j < je; j += kPT) {
+            sq[j - jb] = __ldg(P.lqv + j);
+            sqs[j - jb] = __ldg(P.lqsv + j);
+        }
+    __syncthreads();
+    if (t >= P.M) return;
+    const long long i = P.lperm[(long long)sp * P.M + t];
+    const int u = (int)((long long)sp * P.M + i);
+    RowPt<COST, DP> rp;
+    rp.load(P, i, true);
+    const double w = A.w;
+    const float w_lo = (float)w * (1.f - 0x1p-19f);
+    double mx = -INFINITY, sm = 0.0;
+    int jm = -1;
+    const int js = P.jstar[i];
+    if (js >= 0 && js < P.N) {
+        const double D = dist_global<COST, DP>(P, rp, i, js);
+        mx = fma(-w, D, P.lqv[js]);
+        jm = js;
     }
-    const double R = block_reduce_sum(v0, red);
-    const double DM = block_reduce_max(v1, red);
-    if (tid == 0) {
-        A.st[0] = R;
-        A.st[1] = DM;
-        if (A.count_sweep) A.ctl[1] += 1;
-        skip_switch(P, w_lo);
-        if (A.test_tol && A.sink_tol && R <= *A.sink_tol) {
-            A.ctl[0] = 1;     // converged at the starting iterate: roll back this update
-            A.ctl[2] = 1;
+    const float thr0 = thr_lo_of(mx - kLseCut);
+    const int cnt = P.lcnt[u];
+    const float B = P.lB[i], dq = P.ldqs[sp];
+    const double ub = (double)B + (double)ulpf_of(B) + (double)dq;
+    if (!(cnt >= 0 && thr0 != -INFINITY && dq != INFINITY &&
+          ub + 1e-12 * (fabs((double)B) + fabs((double)dq)) <= (double)thr0)) {
+        P.lq[atomicAdd(P.lctl + 8, 1)] = u;          // certificate failed: dense scan (fallback kernel)
+        return;
+    }
+    // the dense pass's sequence: per chunk the start threshold, survivors in column order
+    // taken two at a time (a chunk's odd last survivor alone), reference updates
+    long long cur = -1;
+    float thr32 = thr0;
+    int pj = -1, nsurv = 0;
+    double px = 0.0;                                 // a pending survivor (first of a pair): its x
+    auto step = [&](int j1, double x1, int j2, double x2, bool two) {
+        if (fmax(x1, x2) > mx + 1.0) {
+            const bool first = x1 >= x2;
+            const double xn = first ? x1 : x2;
+            sm = sm * pexp_lean(fmax(-745.0, mx - xn), thi, tlo);
+            mx = xn;
+            jm = first ? j1 : j2;
+        }
+        const double e1 = pexp_lean(fmax(-745.0, x1 - mx), thi, tlo);
+        const double e2 = pexp_lean(fmax(-745.0, x2 - mx), thi, tlo);
+        sm += two ? e1 + e2 : e1;
+    };
+    // Batches of kLB entries: the loads are independent of the running state and go
+    // first; the fp32 test is branch-free (entries of a chunk that began in an earlier
+    // batch keep its start threshold).  If no survivor of the batch (nor the pending one)
+    // exceeds mx + 1, the reference cannot move inside the batch, so every exponential
+    // is taken against the same mx -- independently, with full ILP -- and the survivors
+    // are then summed in the dense pass's pair order.  Otherwise the batch runs the
+    // sequential pair steps.  Both give the dense pass's bits.
+    const LDT<COST> *lD = reinterpret_cast<const LDT<COST> *>(P.lD) + (long long)u * P.lcap;
+    const int *lj = P.lj + (long long)u * P.lcap;
+    int *tj = sj + threadIdx.x;
+    double *tx = sx + threadIdx.x, *te = se + threadIdx.x;
+    // whole batches (lists are padded to multiples of kLB), 16-byte loads, the next
+    // batch's loads in flight while this one is processed
+    int jn[kLB];
+    LDT<COST> dn[kLB];
+    auto load_batch = [&](int k0) {
+        const int4 a0 = __ldg(reinterpret_cast<const int4 *>(lj + k0));
+        const int4 a1 = __ldg(reinterpret_cast<const int4 *>(lj + k0) + 1);
+        jn[0] = a0.x; jn[1] = a0.y; jn[2] = a0.z; jn[3] = a0.w;
+        jn[4] = a1.x; jn[5] = a1.y; jn[6] = a1.z; jn[7] = a1.w;
+        if constexpr (sizeof(LDT<COST>) == 4) {
+            const float4 d0 = __ldg(reinterpret_cast<const float4 *>(lD + k0));
+            const float4 d1 = __ldg(reinterpret_cast<const float4 *>(lD + k0) + 1);
+            dn[0] = d0.x; dn[1] = d0.y; dn[2] = d0.z; dn[3] = d0.w;
+            dn[4] = d1.x; dn[5] = d1.y; dn[6] = d1.z; dn[7] = d1.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < kLB; q += 2) {
+                const double2 d = __ldg(reinterpret_cast<const double2 *>(lD + k0 + q));
+                dn[q] = d.x;
+                dn[q + 1] = d.y;
+            }
+        }
+    };
+    if (cnt > 0) load_batch(0);
+    for (int k0 = 0; k0 < cnt; k0 += kLB) {
+        int jv[kLB];
+        LDT<COST> dv[kLB];
+        float qsv[kLB];
+        double xv[kLB];
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) { jv[q] = jn[q]; dv[q] = dn[q]; }
+        if (k0 + kLB < cnt) load_batch(k0 + kLB);
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) {
+            if constexpr (STG) {
+                qsv[q] = sqs[jv[q] - jb];
+                xv[q] = fma(-w, (double)dv[q], sq[jv[q] - jb]);
+            } else {
+                qsv[q] = __ldg(P.lqsv + jv[q]);
+                xv[q] = fma(-w, (double)dv[q], __ldg(P.lqv + jv[q]));
+            }
+        }
+        const int nb = min(kLB, cnt - k0);
+        unsigned mask = 0u;
+        const float tnew = thr_lo_of(mx - kLseCut);
+        double xmax = pj >= 0 ? px : -INFINITY;
+#pragma unroll
+        for (int q = 0; q < kLB; ++q) {
+            const float v = fmaf(-w_lo, (float)dv[q], qsv[q]);
+            const float th = (jv[q] >> 5) == cur ? thr32 : tnew;
+            const bool sv = q < nb && v > th;
+            mask |= sv ? (1u << q) : 0u;
+            xmax = sv ? fmax(xmax, xv[q]) : xmax;
+            tj[q * kPT] = jv[q];
+            tx[q * kPT] = xv[q];
+        }
+        if (mask == 0u) continue;
+        if (!(xmax > mx + 1.0)) {
+            // fast path: the reference stays; all exponentials against mx
+            double epend = 0.0;
+            if (pj >= 0) epend = pexp_lean(fmax(-745.0, px - mx), thi, tlo);
+#pragma unroll
+            for (int q = 0; q < kLB; ++q) te[q * kPT] = pexp_lean(fmax(-745.0, xv[q] - mx), thi, tlo);
+            nsurv += __popc(mask);
+            while (mask) {
+                const int q = __ffs(mask) - 1;
+                mask &= mask - 1u;
+                const int jq = tj[q * kPT];
+                const double eq = te[q * kPT];
+                if ((jq >> 5) != cur) {
+                    if (pj >= 0) { sm += epend; pj = -1; }       // the previous chunk's odd survivor
+                    cur = jq >> 5;
+                    thr32 = tnew;
+                }
+                if (pj >= 0) { sm += epend + eq; pj = -1; }
+                else { pj = jq; px = tx[q * kPT]; epend = eq; }
+            }
+            continue;
+        }
+        // a reference update may happen inside this batch: the dense pass's steps in order
+        while (mask) {
+            const int q = __ffs(mask) - 1;
+            mask &= mask - 1u;
+            const int jq = tj[q * kPT];
+            if ((jq >> 5) != cur) {
+                if (pj >= 0) { step(pj, px, pj, px, false); pj = -1; }
+                cur = jq >> 5;
+                thr32 = thr_lo_of(mx - kLseCut);
+                if (thr32 != tnew) {
+                    // mx moved: this and the later entries of the batch are tested against
+                    // the new chunk thresholds, as the dense pass does
+                    unsigned m2 = 0u;
+#pragma unroll
+                    for (int r = 0; r < kLB; ++r) {
+                        const float v = fmaf(-w_lo, (float)dv[r], qsv[r]);
+                        m2 |= (r < nb && r >= q && v > thr32) ? (1u << r) : 0u;
+                    }
+                    mask = m2 & ~((2u << q) - 1u);
+                    if (!((m2 >> q) & 1u)) continue;
+                }
+            }
+            ++nsurv;
+            const double xq = tx[q * kPT];
+            if (pj >= 0) { step(pj, px, jq, xq, true); pj = -1; }
+            else { pj = jq; px = xq; }
         }
     }
+    if (pj >= 0) step(pj, px, pj, px, false);
+    if (A.count_surv && nsurv) atomicAdd(g_surv, (unsigned long long)nsurv);
+    P.pa[(long long)sp * P.M + i] = mx;
+    P.pb[(long long)sp * P.M + i] = sm;
+    P.pj[(long long)sp * P.M + i] = jm;
+}
+
+// Dense scan of the units whose certificate failed: one warp per unit, lane = column
+// of a chunk; the survivors of a chunk are taken in order, two at a time, by every
+// lane alike (values broadcast by shuffles) -- the dense pass's arithmetic.
+template <int COST, int DP>
+__global__ void __launch_bounds__(kPT) lse_fallback_kernel(PassArgs A) {
+    __shared__ double thi[64], tlo[64];
+    if (A.check_done && A.ctl[0]) return;
+    const PassSide &P = A.side[0];
+    if (P.lctl[2 + P.lori] == A.lt) return;
+    const int nq = P.lctl[8];
+    if (nq == 0) return;
+    load_exp_table(A.tab, thi, tlo);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long gw = ((long long)blockIdx.x * kPT + threadIdx.x) >> 5, nw = (long long)gridDim.x * (kPT / 32);
+    const double w = A.w;
+    const float w_lo = (float)w * (1.f - 0x1p-19f);
+    for (long long qi = gw; qi < nq; qi += nw) {
+        const int u = P.lq[qi];
+        const long long i = u % P.M;
+        const int sp = (int)(u / P.M);
+        long long jb, je;
+        split_range(P.N, P.S, sp, jb, je);
+        RowPt<COST, DP> rp;
+        rp.load(P, i, true);
+        double mx = -INFINITY, sm = 0.0;
+        int jm = -1, nsurv = 0;
+        const int js = P.jstar[i];
+        if (js >= 0 && js < P.N) {
+            const double D = dist_global<COST, DP>(P, rp, i, js);
+            mx = fma(-w, D, P.lqv[js]);
+            jm = js;
+        }
+        for (long long j0 = jb; j0 < je; j0 += kCC) {
+            const long long j = j0 + lane;
+            double D = 0.0, q = 0.0;
+            float v = -INFINITY;
+            if (j < je) {
+                D = dist_global<COST, DP>(P, rp, i, j);
+                q = __ldg(P.lqv + j);
+                v = fmaf(-w_lo, (float)D, __ldg(P.lqsv + j));
+            }
+            const float thr32 = thr_lo_of(mx - kLseCut);
+            unsigned mask = __ballot_sync(0xffffffffu, v > thr32);
+            nsurv += __popc(mask);
+            while (mask) {
+                const int c1 = __ffs(mask) - 1;
+                mask &= mask - 1u;
+                const bool two = mask != 0u;
+                const int c2 = two ? __ffs(mask) - 1 : c1;
+                mask &= two ? mask - 1u : mask;
+                const double D1 = __shfl_sync(0xffffffffu, D, c1), q1 = __shfl_sync(0xffffffffu, q, c1);
+                const double D2 = __shfl_sync(0xffffffffu, D, c2), q2 = __shfl_sync(0xffffffffu, q, c2);
+                const double x1 = fma(-w, D1, q1);
+                const double x2 = fma(-w, D2, q2);
+                if (fmax(x1, x2) > mx + 1.0) {
+                    const bool first = x1 >= x2;
+                    const double xn = first ? x1 : x2;
+                    sm = sm * pexp_lean(fmax(-745.0, mx - xn), thi, tlo);
+                    mx = xn;
+                    jm = (int)(j0 + (first ? c1 : c2));
+                }
+                const double e1 = pexp_lean(fmax(-745.0, x1 - mx), thi, tlo);
+                const double e2 = pexp_lean(fmax(-745.0, x2 - mx), thi, tlo);
+                sm += two ? e1 + e2 : e1;
+            }
+        }
+        if (lane == 0) {
+            if (A.count_surv && nsurv) atomicAdd(g_surv, (unsigned long long)nsurv);
+            P.pa[(long long)sp * P.M + i] = mx;
+            P.pb[(long long)sp * P.M + i] = sm;
+            P.pj[(long long)sp * P.M + i] = jm;
+        }
+    }
+}
+
+// the sparse path's merge: one CTA per row block, then the launch finalize
+__global__ void __launch_bounds__(kPT) lse_merge_kernel(PassArgs A) {
+    __shared__ double thi[64], tlo[64];
+    __shared__ double red[kPT / 32];
+    __shared__ bool flag;
+    if (A.check_done && A.ctl[0]) return;
+    const PassSide &P = A.side[0];
+    if (P.lctl[2 + P.lori] == A.lt) return;
+    load_exp_table(A.tab, thi, tlo);
+    __syncthreads();
+    const int rb = blockIdx.x;
+    const long long i = (long long)rb * kPT + threadIdx.x;
+    const float w_lo = (float)A.w * (1.f - 0x1p-19f);
+    lse_rowblock_finalize(A, P, rb, i, i < P.M, thi, tlo, red, &flag, w_lo, false, true);
 }
 
 // =========================================================================

@@ -598,3 +598,80 @@ def test_solve_is_bit_reproducible(P, name, scale):
     assert r1["obj"] == r2["obj"] and r1["cg_iters"] == r2["cg_iters"]
     for k in ("f", "g", "phi", "psi", "u", "v"):
         assert np.array_equal(H(r1[k]), H(r2[k])), k
+
+
+@pytest.mark.parametrize("name,mk", [("c3s", lambda: make("c3_gmm10k", scale=0.05)),
+                                     ("c4s", lambda: make("c4_l1rect", scale=0.04)),
+                                     ("c1t", lambda: make("c1_rand1k", scale=0.125)),
+                                     ("rag_dense", lambda: ragged(37, 1029, 5)),
+                                     ("c3rs", lambda: make("c3_gmm10k_r", scale=0.03)),
+                                     ("rag_l1_r", lambda: ragged(133, 47, 17, "l1", 3, real=True)),
+                                     ("rag_sq", lambda: ragged(301, 517, 9, "sq", 10))])
+def test_sparse_sweeps_bit_identical(P, name, mk, monkeypatch):
+    # The Sinkhorn phase walks certified candidate lists (lse_sparse_kernel) instead of the
+    # dense m x n block; the certificate proves that no entry outside a list can pass the
+    # dense pass's fp32 test, and the lists are walked with the dense pass's chunk
+    # thresholds and survivor pairing -- so f, g and the sweep count must be bit-identical
+    # to the dense sweeps.  The third setting forces list overflow (capacity 2: regrowth)
+    # and failing certificates (margin 0.01: dense fallback rows and re-records).
+    w = mk()
+    out = []
+    for k in (0, 1):
+        if k == 0:
+            phi, psi, s = w.eta * np.log(w.a), w.eta * np.log(w.b), 1.0
+            f, g = np.zeros(w.m), np.zeros(w.n)
+        else:
+            C, Ck, phi, psi, s, f, g = oracle_state(w, 1)
+            f = f + np.random.default_rng(3).normal(0, 3 * w.eta, w.m)
+        res = []
+        for env in ({}, {"PINS_SPARSE_SWEEP": "1"},
+                    {"PINS_SPARSE_SWEEP": "1", "PINS_LIST_CAP": "2", "PINS_LIST_MARGIN": "0.01"}):
+            for key in ("PINS_SPARSE_SWEEP", "PINS_LIST_CAP", "PINS_LIST_MARGIN"):
+                monkeypatch.delenv(key, raising=False)
+            for key, v in env.items():
+                monkeypatch.setenv(key, v)
+            pb = P.DeviceProblem.from_workload(w)
+            ws = P.Workspace()
+            fd, gd = T(f), T(g)
+            t, r = P.sinkhorn(ws, pb, T(phi), T(psi), s, fd, gd, 0.0, 70)
+            t2, r2 = P.sinkhorn(ws, pb, T(phi), T(psi), s, fd, gd, 1e-3, 400)   # stops on the tolerance
+            res.append((t, r, t2, r2, H(fd), H(gd)))
+        d = res[0]
+        for o in res[1:]:
+            assert o[0] == d[0] and o[2] == d[2], (name, k, o[:4], d[:4])
+            assert o[1] == d[1] and o[3] == d[3]
+            assert np.array_equal(o[4], d[4]) and np.array_equal(o[5], d[5])
+        out.append(d[2])
+    # and whole solves
+    objs = []
+    for env in ({}, {"PINS_SPARSE_SWEEP": "1"}):
+        for key in ("PINS_SPARSE_SWEEP", "PINS_LIST_CAP", "PINS_LIST_MARGIN"):
+            monkeypatch.delenv(key, raising=False)
+        for key, v in env.items():
+            monkeypatch.setenv(key, v)
+        pb = P.DeviceProblem.from_workload(w)
+        r = P.solve(pb, P.default_params(K=5, outer_tol=0.0))
+        objs.append((r["obj"], r["sweeps"], H(r["u"]), H(r["v"])))
+    assert objs[0][0] == objs[1][0] and objs[0][1] == objs[1][1]
+    assert np.array_equal(objs[0][2], objs[1][2]) and np.array_equal(objs[0][3], objs[1][3])
+
+
+@pytest.mark.parametrize("name,scale", [("c4_l1rect", 0.04), ("c3_gmm10k", 0.05), ("c1_rand1k", 0.2)])
+def test_no_uninitialised_reads(P, name, scale, monkeypatch):
+    # every device buffer the library allocates is filled with a garbage byte first
+    # (PINS_POISON, dev switch): a solve that read memory before writing it would change
+    # (or fault); results must be bit-identical to the unpoisoned solve.  (Regression: the
+    # tree workspace was once reallocated at the same address and its stale factor reused.)
+    w = make(name, scale=scale)
+    out = []
+    for z in (None, "165", "0"):
+        monkeypatch.delenv("PINS_POISON", raising=False)
+        if z is not None:
+            monkeypatch.setenv("PINS_POISON", z)
+        pb = P.DeviceProblem.from_workload(w)
+        r = P.solve(pb, P.default_params(K=4, outer_tol=0.0))
+        out.append((r["obj"], r["cg_iters"], r["sweeps"], H(r["u"]), H(r["v"]), H(r["f"])))
+    for o in out[1:]:
+        assert o[0] == out[0][0] and o[1] == out[0][1] and o[2] == out[0][2]
+        for x, y in zip(o[3:], out[0][3:]):
+            assert np.array_equal(x, y)
