@@ -130,6 +130,7 @@ class ClockSampler:
 # I1 issue slots; per SURVIVOR (entry evaluated exactly) the fp64 exponential and its
 # accumulation cost I2 issue slots, F2 of them on the FP64 pipe (half the FP32 rate on
 # B200: 64 lanes/clk/SM).  Survivors are counted on the device (pins_prof_read_work).
+SWEEP_CLASSES = ("sweep_row", "sweep_col", "ksweep", "sweep_aux")
 ALU_MODEL = {"sweep_row": dict(I1=6, I2=24, F2=16), "eval": dict(I1=6, I2=30, F2=19)}
 
 
@@ -169,6 +170,15 @@ def kernel_roofline(cls: str, w, launches: int, ms: float, clocks_mhz: float, pe
                 f"({surv / entries:.3f})",
                 "peak_source": f"derived (DESIGN.md §7): I1={md['I1']}, I2={md['I2']}, F2={md['F2']} per "
                                f"entry / survivor, 148 SM x 128 issue lanes (64 FP64) x {clocks_mhz:.0f} MHz"}
+    if cls == "ksweep":
+        # absorbed kernel-matrix half-sweep (ELL walk): streams 12 B per listed entry
+        # (int32 column + fp64 kernel value); `work` = entries walked, counted on the device
+        byts = 12.0 * work / max(1, launches)
+        ach = byts / avg_s / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        return {"kernel": cls, "bound": "hbm", "unit": "GB/s", "achieved": ach, "peak": peak, "frac": ach / peak,
+                "work_per_launch": f"{byts:.3g} B (12 B x {work / max(1, launches):.3g} listed entries)",
+                "peak_source": f"{src} HBM copy"}
     if cls == "cg":
         byts = work / max(1, launches)
         ach = byts / avg_s / 1e9
@@ -310,7 +320,7 @@ def prof_stats(pins, w, prof, clocks_mhz, peaks, steps):
     """Per-class device time, launches, and roofline entries of a profiled region."""
     total_ms = sum(v["ms"] for v in prof.values())
     kerns = {}
-    for c in ("sweep_row", "sweep_col", "eval", "cg"):
+    for c in ("sweep_row", "sweep_col", "ksweep", "eval", "cg"):
         if prof[c]["launches"] and prof[c]["ms"] > 0:
             cls = "sweep_row" if c == "sweep_col" else c
             e = kernel_roofline(cls, w, prof[c]["launches"], prof[c]["ms"], clocks_mhz, peaks, prof[c]["work"])
@@ -343,11 +353,13 @@ def config_lines(pins, prm, peaks, mhz):
         sec = e0.elapsed_time(e1) / 1e3
         pins.prof_reset()
         pins.prof_enable(True)
-        pins.solve(pb, prm, want_duals=False, ws=ws)
+        r2 = pins.solve(pb, prm, want_duals=False, ws=ws)
         pins.prof_enable(False)
         prof = pins.prof_read()
-        sw_l = prof["sweep_row"]["launches"] + prof["sweep_col"]["launches"]
-        sw_ms = prof["sweep_row"]["ms"] + prof["sweep_col"]["ms"]
+        # every launch of the Sinkhorn phases: dense half-sweeps, ELL walks, and the list
+        # modes' auxiliary launches (records, sort, ELL build, fallback, merge)
+        sw_ms = sum(prof[c]["ms"] for c in SWEEP_CLASSES)
+        sw_l = 2 * r2["sweeps"]
         kerns = prof_stats(pins, w, prof, mhz, peaks, 1)
         cg = kerns.get("cg", {})
         out[name] = {
@@ -359,8 +371,12 @@ def config_lines(pins, prm, peaks, mhz):
             "rel_err": None if gold is None else abs(r["obj"] - gold) / abs(gold),
             "sweeps_per_s": (sw_l / 2) / (sw_ms / 1e3) if sw_ms > 0 else None,
             "half_sweep_us": sw_ms / sw_l * 1e3 if sw_l else None,
-            "half_sweep_roofline": {k: kerns["sweep_row"][k] for k in ("bound", "achieved", "peak", "unit", "frac")}
+            "half_sweep_roofline": {k: kerns["sweep_row"][k] for k in ("bound", "achieved", "peak", "unit", "frac",
+                                                                         "avg_launch_us", "launches")}
             if "sweep_row" in kerns else None,
+            "ksweep_roofline": {k: kerns["ksweep"][k] for k in ("bound", "achieved", "peak", "unit", "frac",
+                                                                  "avg_launch_us", "launches")}
+            if "ksweep" in kerns else None,
             "cg_spmv_gbs": cg.get("achieved"), "cg_frac_hbm": cg.get("frac"),
         }
         del ws
@@ -391,6 +407,7 @@ def hbm_section(pins, peaks):
     f = torch.zeros(w.m, dtype=torch.float64, device="cuda")
     g = torch.zeros(w.n, dtype=torch.float64, device="cuda")
     ws = pins.Workspace()
+    os.environ["PINS_KSWEEP"] = "0"                           # the dense half-sweeps themselves
     pins.sinkhorn(ws, pb, phi, psi, s, f, g, 0.0, 3)          # warm-up (and the argmax seeds)
     pins.prof_reset()
     pins.prof_enable(True)
@@ -399,6 +416,27 @@ def hbm_section(pins, peaks):
     pins.evaluate(ws, pb, phi, psi, s, f, g, tau=0.0)        # sums only: the C stream
     pins.prof_enable(False)
     prof = pins.prof_read()
+    del os.environ["PINS_KSWEEP"]
+    # the same phase continued with the absorbed kernel-matrix sweeps (the default of long
+    # phases): ELL walks stream 12 B per listed entry
+    pins.sinkhorn(ws, pb, phi, psi, s, f, g, 0.0, 30)         # records, list capacity growth
+    pins.prof_reset()
+    pins.prof_enable(True)
+    nks = 60
+    pins.sinkhorn(ws, pb, phi, psi, s, f, g, 0.0, nks)
+    pins.prof_enable(False)
+    prof_k = pins.prof_read()
+    L, ms = prof_k["ksweep"]["launches"], prof_k["ksweep"]["ms"]
+    if L and ms > 0:
+        byk = 12.0 * prof_k["ksweep"]["work"] / L
+        gbs = byk / (ms / L / 1e3) / 1e9
+        aux = prof_k["sweep_aux"]["ms"] + prof_k["sweep_row"]["ms"] + prof_k["sweep_col"]["ms"]
+        out["ksweep"] = {"launches": L, "avg_launch_us": ms / L * 1e3, "achieved": gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / peak, "bytes_per_launch": byk, "entries_per_launch": byk / 12.0,
+                         "half_sweep_us_all_launches": (ms + aux) / (2 * nks) * 1e3,
+                         "config": f"the same dense-C instance, {nks} sweeps of one phase in kernel-matrix mode "
+                                   "(dense sweeps, records, ELL builds, fallback and merge launches included in "
+                                   "half_sweep_us_all_launches)"}
     pins.prof_reset()
     pins.prof_enable(True)
     ev = pins.evaluate(ws, pb, phi, psi, s, f, g, tau=1e-4 / (w.m * w.n))   # + sparsify

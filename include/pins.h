@@ -284,7 +284,9 @@ int pins_solve_host(const pins_problem *pb_host, const pins_params *prm, pins_re
 #define PINS_PROF_CG 5          /* conjugate gradient                          */
 #define PINS_PROF_VEC 6         /* small vector kernels                        */
 #define PINS_PROF_PLAN 7        /* dense plan materialisation                  */
-#define PINS_PROF_NCLASS 8
+#define PINS_PROF_KSWEEP 8      /* absorbed kernel-matrix half-sweep (ELL walk)   */
+#define PINS_PROF_SWEEP_AUX 9   /* list modes: record passes (incl. their no-op launches), sort, ELL build, fallback, merge */
+#define PINS_PROF_NCLASS 10
 void pins_prof_enable(int32_t on);
 void pins_prof_reset(void);
 int pins_prof_read(int32_t cls, int64_t *launches, double *ms);
@@ -293,7 +295,9 @@ int pins_prof_read(int32_t cls, int64_t *launches, double *ms);
  * (m + n) per iteration, counted by the host); for PINS_PROF_SWEEP_ROW (all
  * half-sweeps) and PINS_PROF_EVAL (sum passes) the number of plan entries that
  * survived the skip test and were evaluated exactly (counted on the device
- * while profiling is enabled; synchronises); 0 for other classes.           */
+ * while profiling is enabled; synchronises); for PINS_PROF_KSWEEP the listed
+ * entries the ELL walks read (12 B each: int32 column + fp64 kernel value);
+ * 0 for other classes.                                                      */
 int pins_prof_read_work(int32_t cls, double *work);
 
 #ifdef __cplusplus

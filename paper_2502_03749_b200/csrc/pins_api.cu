@@ -106,17 +106,18 @@ struct ProfScope {
 extern "C" void pins_prof_enable(int32_t on) { g_prof.on = on != 0; }
 extern "C" void pins_prof_reset(void) {
     g_prof.fold();
-    const unsigned long long z[2] = {0, 0};
+    const unsigned long long z[3] = {0, 0, 0};
     cudaMemcpyToSymbol(pins::g_surv, z, sizeof z);
     for (int c = 0; c < PINS_PROF_NCLASS; ++c) { g_prof.launches[c] = 0; g_prof.ms[c] = 0.0; g_prof.work[c] = 0.0; }
 }
 extern "C" int pins_prof_read_work(int32_t cls, double *work) {
     PINS_ARG(cls >= 0 && cls < PINS_PROF_NCLASS && work, "class / pointer");
     *work = g_prof.work[cls];
-    if (cls == PINS_PROF_SWEEP_ROW || cls == PINS_PROF_EVAL) {     // survivors counted on the device
-        unsigned long long sv[2] = {0, 0};
+    if (cls == PINS_PROF_SWEEP_ROW || cls == PINS_PROF_EVAL || cls == PINS_PROF_KSWEEP) {
+        // counted on the device: survivors (dense passes), listed entries walked (ELL walk)
+        unsigned long long sv[3] = {0, 0, 0};
         PINS_CUDA(cudaMemcpyFromSymbol(sv, pins::g_surv, sizeof sv));
-        *work = (double)sv[cls == PINS_PROF_SWEEP_ROW ? 0 : 1];
+        *work = (double)sv[cls == PINS_PROF_SWEEP_ROW ? 0 : cls == PINS_PROF_EVAL ? 1 : 2];
     }
     return PINS_OK;
 }
@@ -182,6 +183,8 @@ struct SideBufs {
     DevBuf pa, pb, pj, psc, blk, blkoff, ticket, cnt, bcol, bval, jstar;
     // certified candidate lists of the Sinkhorn phase (pins_pass.cuh lse_sparse_kernel)
     DevBuf lcnt, lj, lD, lB, lqref, lqv, lqsv, ldqc, ldqs, lperm, lq;
+    // absorbed kernel-matrix sweeps (lse_ksweep_kernel): sliced-ELL copy of the lists
+    DevBuf lqd, lmref, ellj, ellK;
 };
 
 struct pins_workspace {
@@ -636,17 +639,21 @@ size_t pass_smem(K kern, size_t bytes) {
     LAUNCH(PINS_PROF_EVAL, st, sum_pass_kernel<C0_, C1_, DP_><<<grid, kPT,                                    \
            pass_smem(sum_pass_kernel<C0_, C1_, DP_>, kTma<C0_> ? kTmaSmem : 0), st>>>(A, tm0, tm1))
 
-cudaError_t launch_lse(int cost, int dp, int grid, cudaStream_t st, const PassArgs &A, const CUtensorMap &tm) {
+// pcls >= 0: the profiler class of this launch (list modes book their record passes, most
+// of which exit at once, under PINS_PROF_SWEEP_AUX)
+cudaError_t launch_lse(int cost, int dp, int grid, cudaStream_t st, const PassArgs &A, const CUtensorMap &tm,
+                       int pcls = -1) {
+    const int crow = pcls >= 0 ? pcls : PINS_PROF_SWEEP_ROW, ccol = pcls >= 0 ? pcls : PINS_PROF_SWEEP_COL;
     switch (cost) {
-        case PC_DENSE_ROW: LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_DENSE_ROW, 4); break;
-        case PC_DENSE_COL: LSE_LAUNCH(PINS_PROF_SWEEP_COL, PC_DENSE_COL, 4); break;
-        case PC_DENSE_ROW_T: LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_DENSE_ROW_T, 4); break;
-        case PC_DENSE_COL_T: LSE_LAUNCH(PINS_PROF_SWEEP_COL, PC_DENSE_COL_T, 4); break;
-        case PC_SQ32: PINS_DP_DISPATCH(dp, LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_SQ32, DP)); break;
-        case PC_L132: PINS_DP_DISPATCH(dp, LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_L132, DP)); break;
-        case PC_SQ64: PINS_DP_DISPATCH(dp, LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_SQ64, DP)); break;
-        case PC_SQTC: PINS_DP_DISPATCH(dp, LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_SQTC, DP)); break;
-        default: PINS_DP_DISPATCH(dp, LSE_LAUNCH(PINS_PROF_SWEEP_ROW, PC_L164, DP)); break;
+        case PC_DENSE_ROW: LSE_LAUNCH(crow, PC_DENSE_ROW, 4); break;
+        case PC_DENSE_COL: LSE_LAUNCH(ccol, PC_DENSE_COL, 4); break;
+        case PC_DENSE_ROW_T: LSE_LAUNCH(crow, PC_DENSE_ROW_T, 4); break;
+        case PC_DENSE_COL_T: LSE_LAUNCH(ccol, PC_DENSE_COL_T, 4); break;
+        case PC_SQ32: PINS_DP_DISPATCH(dp, LSE_LAUNCH(crow, PC_SQ32, DP)); break;
+        case PC_L132: PINS_DP_DISPATCH(dp, LSE_LAUNCH(crow, PC_L132, DP)); break;
+        case PC_SQ64: PINS_DP_DISPATCH(dp, LSE_LAUNCH(crow, PC_SQ64, DP)); break;
+        case PC_SQTC: PINS_DP_DISPATCH(dp, LSE_LAUNCH(crow, PC_SQTC, DP)); break;
+        default: PINS_DP_DISPATCH(dp, LSE_LAUNCH(crow, PC_L164, DP)); break;
     }
     return cudaGetLastError();
 }
@@ -704,6 +711,35 @@ cudaError_t launch_lse_sparse(int cost, int dp, int grid, int gfb, int gmerge, s
     return cudaGetLastError();
 }
 
+constexpr size_t kKSmemMax = 200 * 1024;     // lse_ksweep_kernel: the widest split's u_j (8 B per column)
+
+// the absorbed kernel-matrix path of a half-sweep: ELL build (only right after a record),
+// ELL walk, dense fallback of failed units, merge
+cudaError_t launch_lse_k(int cost, int dp, int grid, int gfb, int gmerge, size_t smem, cudaStream_t st,
+                         const PassArgs &A) {
+    const bool f32 = cost == PC_SQTC || cost == PC_SQ32 || cost == PC_L132;
+    if (f32) LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_kbuild_kernel<float><<<grid, kPT, 0, st>>>(A));
+    else LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_kbuild_kernel<double><<<grid, kPT, 0, st>>>(A));
+#define LSK_LAUNCH(C_, DP_)                                                                     \
+    do {                                                                                        \
+        LAUNCH(PINS_PROF_KSWEEP, st, lse_ksweep_kernel<C_, DP_><<<grid, kPT,                 \
+               (pass_smem(lse_ksweep_kernel<C_, DP_>, kKSmemMax), smem), st>>>(A));             \
+        LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_fallback_k_kernel<C_, DP_><<<gfb, kPT, 0, st>>>(A)); \
+        LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_merge_kernel<<<gmerge, kPT, 0, st>>>(A));           \
+    } while (0)
+    switch (cost) {
+        case PC_DENSE_ROW: case PC_DENSE_ROW_T: LSK_LAUNCH(PC_DENSE_ROW_T, 4); break;
+        case PC_DENSE_COL: case PC_DENSE_COL_T: LSK_LAUNCH(PC_DENSE_COL_T, 4); break;
+        case PC_SQ32: PINS_DP_DISPATCH(dp, LSK_LAUNCH(PC_SQ32, DP)); break;
+        case PC_L132: PINS_DP_DISPATCH(dp, LSK_LAUNCH(PC_L132, DP)); break;
+        case PC_SQ64: PINS_DP_DISPATCH(dp, LSK_LAUNCH(PC_SQ64, DP)); break;
+        case PC_SQTC: PINS_DP_DISPATCH(dp, LSK_LAUNCH(PC_SQTC, DP)); break;
+        default: PINS_DP_DISPATCH(dp, LSK_LAUNCH(PC_L164, DP)); break;
+    }
+#undef LSK_LAUNCH
+    return cudaGetLastError();
+}
+
 // candidate-list margin below the LSE cut (units of the exponent): wider lists, fewer
 // record passes
 double list_margin() {
@@ -712,7 +748,7 @@ double list_margin() {
 }
 
 // candidate-list buffers of both sides at capacity ws->lcap per (row, split)
-int ensure_lists(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
+int ensure_lists(pins_workspace *ws, const pins_problem *pb, cudaStream_t st, bool kmode = false) {
     for (int o = 0; o < 2; ++o) {
         const long long M = o == 0 ? pb->m : pb->n, N = o == 0 ? pb->n : pb->m, S = ws->S[o];
         const int cost = o == 0 ? ws->cost_row : ws->cost_col;
@@ -729,6 +765,13 @@ int ensure_lists(pins_workspace *ws, const pins_problem *pb, cudaStream_t st) {
         PINS_TRY(ensure(B.ldqs, sizeof(float) * S));
         PINS_TRY(ensure(B.lperm, sizeof(int) * S * M));
         PINS_TRY(ensure(B.lq, sizeof(int) * S * M));
+        if (kmode) {
+            const long long Mpad = (M + 31) / 32 * 32;
+            PINS_TRY(ensure(B.lqd, sizeof(double) * N));
+            PINS_TRY(ensure(B.lmref, sizeof(double) * S * M));
+            PINS_TRY(ensure(B.ellj, sizeof(int) * S * ws->lcap * Mpad));
+            PINS_TRY(ensure(B.ellK, sizeof(double) * S * ws->lcap * Mpad));
+        }
     }
     PINS_TRY(ensure(ws->lctl, sizeof(int) * 16));
     (void)st;
@@ -779,13 +822,26 @@ int half_sweep(pins_workspace *ws, const pins_problem *pb, int o, const double *
         P.lctl = ptr<int>(ws->lctl);
         A.lt = lt;
         A.lmargin = list_margin();
+        if (lmode == 2) {
+            P.lqd = ptr<double>(B.lqd);
+            P.lmref = ptr<double>(B.lmref);
+            P.ellj = ptr<int>(B.ellj);
+            P.ellK = ptr<double>(B.ellK);
+            P.Mpad = (P.M + 31) / 32 * 32;
+        }
         P.lrec = 1;
-        PINS_CUDA(launch_lse(cost, ws->dp, A.G0, st, A, o == 0 ? ws->tm_row : ws->tm_col));
+        PINS_CUDA(launch_lse(cost, ws->dp, A.G0, st, A, o == 0 ? ws->tm_row : ws->tm_col,
+                             lmode == 2 ? PINS_PROF_SWEEP_AUX : -1));
         P.lrec = 0;
-        LAUNCH(PINS_PROF_SWEEP_ROW, st, lse_sort_kernel<<<P.S, 1024, 0, st>>>(A));
+        LAUNCH(lmode == 2 ? PINS_PROF_SWEEP_AUX : PINS_PROF_SWEEP_ROW, st, lse_sort_kernel<<<P.S, 1024, 0, st>>>(A));
         // the widest split's column values (q fp64 + qs fp32) staged per CTA when they fit
         const long long nch = (P.N + kCC - 1) / kCC, wmax = kCC * ((nch + P.S - 1) / P.S);
         const size_t stage = (size_t)wmax * 12 + 16;
+        if (lmode == 2) {
+            PINS_CUDA(launch_lse_k(cost, ws->dp, (int)(P.S * ((P.M + kPT - 1) / kPT)), 4 * ws->nsm, P.RB,
+                                   (size_t)wmax * 8 + 16, st, A));
+            return PINS_OK;
+        }
         P.lstage = stage <= 64 * 1024 ? 1 : 0;
         PINS_CUDA(launch_lse_sparse(cost, ws->dp, (int)(P.S * ((P.M + kPT - 1) / kPT)), 4 * ws->nsm, P.RB,
                                     P.lstage ? stage : 0, st, A));
@@ -821,28 +877,44 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
     double tolv = prm->sink_tol;
     PINS_CUDA(cudaMemcpyAsync(ws->tol.p, &tolv, sizeof(double), cudaMemcpyHostToDevice, st));
     PINS_CUDA(cudaMemsetAsync(ws->ctl.p, 0, sizeof(int) * 8, st));
-    // certified candidate lists (lse_sparse_kernel): recorded by the first sweep of the
-    // phase and again whenever a certificate fails; bit-identical to the dense sweeps
-    const bool lists = getenv("PINS_SPARSE_SWEEP") != nullptr && prm->T1 > 1;
-    if (lists) {
+    // Candidate lists of the phase.  Mode 1 (PINS_SPARSE_SWEEP, opt-in): the certified list
+    // walk, bit-identical to the dense sweeps.  Mode 2 (default; PINS_KSWEEP=0 switches it
+    // off): absorbed kernel-matrix sweeps (lse_ksweep_kernel), engaged once the phase has
+    // run kstart dense sweeps, so the short phases of the later EPPA iterations never pay
+    // for a record.  Lists are recorded by the first sweep in a list mode and again
+    // whenever too many certificates fail or a list overflows.
+    const bool walk = getenv("PINS_SPARSE_SWEEP") != nullptr && prm->T1 > 1;
+    const int kstart = getenv("PINS_KSWEEP_START") ? atoi(getenv("PINS_KSWEEP_START")) : 7;
+    bool kavail = !walk && prm->T1 > 1 && !(getenv("PINS_KSWEEP") && getenv("PINS_KSWEEP")[0] == '0');
+    for (int o = 0; o < 2 && kavail; ++o) {          // the widest split's u_j must fit in shared memory
+        const long long N = o == 0 ? pb->n : pb->m, nch = (N + kCC - 1) / kCC;
+        const long long wmax = kCC * ((nch + ws->S[o] - 1) / ws->S[o]);
+        if ((size_t)wmax * 8 + 16 > kKSmemMax) kavail = false;
+    }
+    int lmode = 0;
+    auto lists_begin = [&](int mode) -> int {
         if (ws->lcap == 0) ws->lcap = getenv("PINS_LIST_CAP") ? std::max(1LL, atoll(getenv("PINS_LIST_CAP"))) : 64;
-        ws->lcap = (ws->lcap + 7) / 8 * 8;        // lists padded to whole batches of 8
-        PINS_TRY(ensure_lists(ws, pb, st));
+        ws->lcap = (ws->lcap + 15) / 16 * 16;     // lists padded to whole batches (8 walk, 16 ELL)
+        PINS_TRY(ensure_lists(ws, pb, st, mode == 2));
         const int init[16] = {1, 1, -1, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         PINS_CUDA(cudaMemcpyAsync(ws->lctl.p, init, sizeof init, cudaMemcpyHostToDevice, st));
-    }
+        lmode = mode;
+        return PINS_OK;
+    };
+    if (walk) PINS_TRY(lists_begin(1));
     int done = 0, batch = 1, queued = 0, lt = 0;
     int *hc = reinterpret_cast<int *>(ws->h + 40);
     while (!done && queued < prm->T1) {
+        if (kavail && lmode == 0 && queued >= kstart) PINS_TRY(lists_begin(2));
         const int nb = std::min(batch, prm->T1 - queued);
         for (int q = 0; q < nb; ++q) {
             const bool first = (queued + q) == 0;
-            PINS_TRY(half_sweep(ws, pb, 0, phi, psi, s, f, g, true, !first, st, lists ? 1 : 0, lt++));
-            PINS_TRY(half_sweep(ws, pb, 1, phi, psi, s, f, g, true, false, st, lists ? 1 : 0, lt++));
+            PINS_TRY(half_sweep(ws, pb, 0, phi, psi, s, f, g, true, !first, st, lmode, lt++));
+            PINS_TRY(half_sweep(ws, pb, 1, phi, psi, s, f, g, true, false, st, lmode, lt++));
         }
         queued += nb;
         PINS_CUDA(cudaMemcpyAsync(hc, ws->ctl.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
-        if (lists) PINS_CUDA(cudaMemcpyAsync(hc + 4, ws->lctl.p, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
+        if (lmode) PINS_CUDA(cudaMemcpyAsync(hc + 4, ws->lctl.p, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
         PINS_CUDA(cudaStreamSynchronize(st));
         done = hc[0];
         *sweeps_out = hc[1];
@@ -850,16 +922,17 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
             PINS_CUDA(cudaMemcpyAsync(f, ws->fsave.p, sizeof(double) * pb->m, cudaMemcpyDeviceToDevice, st));
         }
         batch = std::min(batch * 2, 64);
-        if (lists && !done && hc[4 + 4] > 0) {
+        if (lmode && !done && hc[4 + 4] > 0) {
             // a list past capacity (its (split, row) scans densely): grow the lists (the
             // stream is idle here) and record them again
-            ws->lcap = (std::max<long long>(2 * ws->lcap, (long long)(1.25 * hc[4 + 5]) + 8) + 7) / 8 * 8;
-            PINS_TRY(ensure_lists(ws, pb, st));
+            ws->lcap = (std::max<long long>(2 * ws->lcap, (long long)(1.25 * hc[4 + 5]) + 8) + 15) / 16 * 16;
+            PINS_TRY(ensure_lists(ws, pb, st, lmode == 2));
             const int init[14] = {1, 1, -1, -1, 0, 0, hc[4 + 6], hc[4 + 7], 0, 0, 0, 0, hc[4 + 12], hc[4 + 13]};
             PINS_CUDA(cudaMemcpyAsync(ws->lctl.p, init, sizeof init, cudaMemcpyHostToDevice, st));
             ++ws->lstat[2];
         }
     }
+    const bool lists = lmode != 0;
     if (lists) {
         ws->lstat[3] += hc[4 + 6] + hc[4 + 7];
         if (getenv("PINS_LIST_STATS"))     // dev instrumentation

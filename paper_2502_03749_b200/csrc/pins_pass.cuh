@@ -169,6 +169,14 @@ struct PassSide {
     int *lperm;                     // [S * M] units by decreasing list length (after each record)
     int *lq;                        // [S * M] units whose certificate failed (fallback queue)
     int lstage;                     // sparse pass: the split's column values staged in shared memory
+    // Absorbed kernel-matrix sweeps (lse_ksweep_kernel): the lists as a sliced-ELL matrix
+    // K_ij = exp(x_ij(record) - lmref) per warp tile of 32 sorted ranks; entry k of lane l of
+    // the tile starting at rank t0 of split sp sits at ((sp * Mpad + t0) * lcap + k * 32 + l
+    double *lqd;                    // [N] the record pass's column values q_j in fp64 (NULL: not kept)
+    double *lmref;                  // [S * M] per unit: the record pass's final reference mx
+    int *ellj;                      // [S * Mpad * lcap] column index inside the split (j - jb)
+    double *ellK;                   // [S * Mpad * lcap] kernel values
+    long long Mpad;                 // M rounded up to whole warp tiles
     // finalize: this side's new potentials are the other side's column values
     double *oqv;                    // [M] q of the other orientation, or NULL
     float *oqsv;                    // [M]
@@ -217,7 +225,7 @@ __device__ __forceinline__ void split_range(long long N, int S, int sp, long lon
 
 // Profiling counters (pins_prof_read_work): entries evaluated in phase 2 (the
 // survivors of the skip test), [0] half-sweeps, [1] sum passes.
-__device__ unsigned long long g_surv[2];
+__device__ unsigned long long g_surv[3];
 
 __device__ __forceinline__ void count_survivors(int on, int slot, int nsurv) {
     if (!on) return;
@@ -1077,7 +1085,11 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
     int lk = 0;
     if (rec && valid && sp == 0) P.lB[i] = lb;
     if (rec && rb == 0)             // the record's column test values (also of chunks skipped below)
-        for (long long j = jb + tid; j < je; j += kPT) P.lqref[j] = qs_of(pot_q(P.gc[j], P.psic[j], inv_eta));
+        for (long long j = jb + tid; j < je; j += kPT) {
+            const double qj = pot_q(P.gc[j], P.psic[j], inv_eta);
+            P.lqref[j] = qs_of(qj);
+            if (P.lqd) P.lqd[j] = qj;
+        }
     const SkipCtx sk = skip_setup(P, rb, sp, i, valid, jb, lb, w_lo, red);
     const TmaRing ring = ring_setup<COST>(dyn_smem, ring_full, &tm0, i0);
     const int nskip = stream_columns<COST, DP>(P, i0, jb, je, inv_eta, 0, false, bufs, &tcs, sk, ring,
@@ -1509,6 +1521,193 @@ __global__ void __launch_bounds__(kPT) lse_merge_kernel(PassArgs A) {
     const long long i = (long long)rb * kPT + threadIdx.x;
     const float w_lo = (float)A.w * (1.f - 0x1p-19f);
     lse_rowblock_finalize(A, P, rb, i, i < P.M, thi, tlo, red, &flag, w_lo, false, true);
+}
+
+// =========================================================================
+// Absorbed kernel-matrix half-sweeps over the certified candidate lists.
+//
+// Inside one Sinkhorn phase the cost term w D_ij of x_ij = q_j - w D_ij is fixed; only
+// the column values q_j move.  With the record pass's values q_j^rec and a per-unit
+// reference r_u (that pass's final mx), every listed entry is
+//     exp(x_ij - r_u - c) = K_ij u_j,   K_ij = exp(q_j^rec - w D_ij - r_u),
+//                                       u_j  = exp(q_j - q_j^rec - c),
+// c = the split's largest column drift (any constant: it only keeps u_j <= ~1).  K is
+// computed once per record (lse_kbuild_kernel, one exponential per listed entry) and
+// stored as a sliced-ELL matrix per warp tile of 32 length-sorted ranks; a half-sweep is
+// then one exponential per COLUMN and one FMA per listed entry -- a sparse
+// matrix-vector product that streams 12 B per entry -- with partials (r_u + c, sum),
+// merged like any other split partial.  The unit certificate of lse_sparse_kernel
+// (unlisted entries are below the LSE cut, R10) is checked per pass; failed units go to
+// lse_fallback_kernel.  Same mathematics as the log-domain pass, different rounding:
+// every term carries a few ulps of relative error instead of the error of x - mx
+// (DESIGN.md section 5).
+// =========================================================================
+constexpr int kKB = 16;                 // ELL entries per lane in flight (loads of one batch)
+
+template <class DT>
+__global__ void __launch_bounds__(kPT) lse_kbuild_kernel(PassArgs A) {
+    __shared__ double thi[64], tlo[64];
+    const PassSide &P = A.side[0];
+    if (P.lctl[2 + P.lori] != A.lt) return;          // only right after a record
+    const int sp = blockIdx.x % P.S, lane = threadIdx.x & 31;
+    const long long t = (long long)(blockIdx.x / P.S) * kPT + threadIdx.x;
+    long long jb, je;
+    split_range(P.N, P.S, sp, jb, je);
+    load_exp_table(A.tab, thi, tlo);
+    __syncthreads();
+    const bool act = t < P.M;
+    long long u = 0;
+    int cnt = 0;
+    double mref = 0.0;
+    if (act) {
+        const long long i = P.lperm[(long long)sp * P.M + t];
+        u = (long long)sp * P.M + i;
+        cnt = max(0, P.lcnt[u]);
+        mref = P.pa[u];                              // the record pass's reference of this unit
+        P.lmref[u] = mref;
+    }
+    // the tile is zero-padded to whole batches of kKB list entries (lcap is a multiple of kKB)
+    const int L = (__reduce_max_sync(0xffffffffu, cnt) + kKB - 1) / kKB * kKB;
+    const long long base = ((long long)sp * P.Mpad + (t & ~31LL)) * P.lcap + lane;
+    const DT *lD = reinterpret_cast<const DT *>(P.lD) + u * P.lcap;
+    const int *lj = P.lj + u * P.lcap;
+    const double w = A.w;
+    for (int k = 0; k < L; ++k) {
+        int jl = 0;
+        double K = 0.0;
+        if (k < cnt) {
+            const int j = lj[k];
+            const double x = fma(-w, (double)lD[k], P.lqd[j]);
+            K = pexp(x - mref, thi, tlo);
+            jl = (int)(j - jb);
+        }
+        P.ellj[base + (long long)k * 32] = jl;
+        P.ellK[base + (long long)k * 32] = K;
+    }
+}
+
+template <int COST, int DP>
+__global__ void __launch_bounds__(kPT) lse_ksweep_kernel(PassArgs A) {
+    extern __shared__ __align__(16) unsigned char lsm[];   // u_j of the split's columns
+    __shared__ double thi[64], tlo[64];
+    if (A.check_done && A.ctl[0]) return;            // Sinkhorn phase already converged
+    const PassSide &P = A.side[0];
+    if (P.lctl[2 + P.lori] == A.lt) return;          // the dense pass recorded this half-sweep
+    const int sp = blockIdx.x % P.S, lane = threadIdx.x & 31;
+    const long long t = (long long)(blockIdx.x / P.S) * kPT + threadIdx.x;
+    long long jb, je;
+    split_range(P.N, P.S, sp, jb, je);
+    load_exp_table(A.tab, thi, tlo);
+    __syncthreads();
+    const float dq = P.ldqs[sp];
+    const double shift = (dq == dq && fabsf(dq) != INFINITY) ? (double)dq : 0.0;
+    double *su = reinterpret_cast<double *>(lsm);
+    for (long long j = jb + threadIdx.x; j < je; j += kPT) {
+        const double q = __ldg(P.lqv + j), qr = __ldg(P.lqd + j);
+        su[j - jb] = (q == -INFINITY || qr == -INFINITY) ? 0.0 : pexp(q - qr - shift, thi, tlo);
+    }
+    __syncthreads();
+    const bool act = t < P.M;
+    long long i = 0, u = 0;
+    int cnt = 0;
+    bool ok = false;
+    if (act) {
+        i = P.lperm[(long long)sp * P.M + t];
+        u = (long long)sp * P.M + i;
+        cnt = P.lcnt[u];
+        // the unit certificate of lse_sparse_kernel: no unlisted entry can pass the LSE cut
+        RowPt<COST, DP> rp;
+        rp.load(P, i, true);
+        double mx = -INFINITY;
+        const int js = P.jstar[i];
+        if (js >= 0 && js < P.N) mx = fma(-A.w, dist_global<COST, DP>(P, rp, i, js), P.lqv[js]);
+        const float thr0 = thr_lo_of(mx - kLseCut);
+        const float B = P.lB[i];
+        const double ub = (double)B + (double)ulpf_of(B) + (double)dq;
+        ok = cnt >= 0 && thr0 != -INFINITY && dq != INFINITY &&
+             ub + 1e-12 * (fabs((double)B) + fabs((double)dq)) <= (double)thr0;
+        if (!ok) P.lq[atomicAdd(P.lctl + 8, 1)] = (int)u;     // dense scan (fallback kernel)
+    }
+    const int L = __reduce_max_sync(0xffffffffu, ok ? cnt : 0);
+    const long long base = ((long long)sp * P.Mpad + (t & ~31LL)) * P.lcap + lane;
+    const int *ej = P.ellj + base;
+    const double *eK = P.ellK + base;
+    // lanes past their own list read the tile's zero padding (K = 0, column 0).  Whole
+    // batches of kKB entries per lane: the loads of a batch are independent and all in
+    // flight together (the longest tiles are a serial chain of L / kKB memory latencies)
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int k = 0; k < L; k += kKB) {
+        int jj[kKB];
+        double KK[kKB];
+#pragma unroll
+        for (int q = 0; q < kKB; ++q) {
+            jj[q] = __ldcs(ej + (k + q) * 32);
+            KK[q] = __ldcs(eK + (k + q) * 32);
+        }
+#pragma unroll
+        for (int q = 0; q < kKB; q += 4) {
+            s0 = fma(KK[q + 0], su[jj[q + 0]], s0);
+            s1 = fma(KK[q + 1], su[jj[q + 1]], s1);
+            s2 = fma(KK[q + 2], su[jj[q + 2]], s2);
+            s3 = fma(KK[q + 3], su[jj[q + 3]], s3);
+        }
+    }
+    if (!ok) return;
+    const double sm = (s0 + s1) + (s2 + s3);
+    if (cnt > 0 && !(sm > 1e-280)) {                 // every listed term underflowed: exact dense scan
+        P.lq[atomicAdd(P.lctl + 8, 1)] = (int)u;
+        return;
+    }
+    if (A.count_surv && cnt) atomicAdd(g_surv + 2, (unsigned long long)cnt);   // ELL entries walked
+    P.pa[u] = cnt > 0 ? P.lmref[u] + shift : -INFINITY;
+    P.pb[u] = sm;
+    P.pj[u] = -1;
+}
+
+// Dense scan of the units whose certificate failed, kernel-matrix mode: one warp per
+// unit, every lane an online log-sum-exp over its columns (j = jb + lane, + 32, ...),
+// combined in lane order.  (The list-walk mode needs the dense pass's survivor sequence
+// -- lse_fallback_kernel; here only the sums matter.)
+template <int COST, int DP>
+__global__ void __launch_bounds__(kPT) lse_fallback_k_kernel(PassArgs A) {
+    __shared__ double thi[64], tlo[64];
+    if (A.check_done && A.ctl[0]) return;
+    const PassSide &P = A.side[0];
+    if (P.lctl[2 + P.lori] == A.lt) return;
+    const int nq = P.lctl[8];
+    if (nq == 0) return;
+    load_exp_table(A.tab, thi, tlo);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long gw = ((long long)blockIdx.x * kPT + threadIdx.x) >> 5, nw = (long long)gridDim.x * (kPT / 32);
+    const double w = A.w;
+    for (long long qi = gw; qi < nq; qi += nw) {
+        const int u = P.lq[qi];
+        const long long i = u % P.M;
+        const int sp = (int)(u / P.M);
+        long long jb, je;
+        split_range(P.N, P.S, sp, jb, je);
+        RowPt<COST, DP> rp;
+        rp.load(P, i, true);
+        double mx = -INFINITY, sm = 0.0;
+        for (long long j = jb + lane; j < je; j += 32) {
+            const double x = fma(-w, dist_global<COST, DP>(P, rp, i, j), __ldg(P.lqv + j));
+            if (x == -INFINITY) continue;
+            if (x > mx) {
+                sm = fma(sm, pexp(mx - x, thi, tlo), 1.0);
+                mx = x;
+            } else {
+                sm += pexp(x - mx, thi, tlo);
+            }
+        }
+        const double Mx = warp_max(mx);
+        const double tot = warp_sum(mx == -INFINITY ? 0.0 : sm * pexp(mx - Mx, thi, tlo));
+        if (lane == 0) {
+            P.pa[(long long)sp * P.M + i] = Mx;
+            P.pb[(long long)sp * P.M + i] = tot;
+            P.pj[(long long)sp * P.M + i] = -1;
+        }
+    }
 }
 
 // =========================================================================

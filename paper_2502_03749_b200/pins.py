@@ -310,7 +310,7 @@ def solve(pb: DeviceProblem, prm: Optional[Params] = None, trace: bool = False, 
     return out
 
 
-PROF_CLASSES = ["sweep_row", "sweep_col", "eval", "reduce", "csr", "cg", "vec", "plan"]
+PROF_CLASSES = ["sweep_row", "sweep_col", "eval", "reduce", "csr", "cg", "vec", "plan", "ksweep", "sweep_aux"]
 
 
 def prof_enable(on: bool = True):

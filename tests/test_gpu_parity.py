@@ -624,9 +624,9 @@ def test_sparse_sweeps_bit_identical(P, name, mk, monkeypatch):
             C, Ck, phi, psi, s, f, g = oracle_state(w, 1)
             f = f + np.random.default_rng(3).normal(0, 3 * w.eta, w.m)
         res = []
-        for env in ({}, {"PINS_SPARSE_SWEEP": "1"},
+        for env in ({"PINS_KSWEEP": "0"}, {"PINS_SPARSE_SWEEP": "1"},
                     {"PINS_SPARSE_SWEEP": "1", "PINS_LIST_CAP": "2", "PINS_LIST_MARGIN": "0.01"}):
-            for key in ("PINS_SPARSE_SWEEP", "PINS_LIST_CAP", "PINS_LIST_MARGIN"):
+            for key in ("PINS_SPARSE_SWEEP", "PINS_LIST_CAP", "PINS_LIST_MARGIN", "PINS_KSWEEP"):
                 monkeypatch.delenv(key, raising=False)
             for key, v in env.items():
                 monkeypatch.setenv(key, v)
@@ -644,8 +644,8 @@ def test_sparse_sweeps_bit_identical(P, name, mk, monkeypatch):
         out.append(d[2])
     # and whole solves
     objs = []
-    for env in ({}, {"PINS_SPARSE_SWEEP": "1"}):
-        for key in ("PINS_SPARSE_SWEEP", "PINS_LIST_CAP", "PINS_LIST_MARGIN"):
+    for env in ({"PINS_KSWEEP": "0"}, {"PINS_SPARSE_SWEEP": "1"}):
+        for key in ("PINS_SPARSE_SWEEP", "PINS_LIST_CAP", "PINS_LIST_MARGIN", "PINS_KSWEEP"):
             monkeypatch.delenv(key, raising=False)
         for key, v in env.items():
             monkeypatch.setenv(key, v)
@@ -654,6 +654,82 @@ def test_sparse_sweeps_bit_identical(P, name, mk, monkeypatch):
         objs.append((r["obj"], r["sweeps"], H(r["u"]), H(r["v"])))
     assert objs[0][0] == objs[1][0] and objs[0][1] == objs[1][1]
     assert np.array_equal(objs[0][2], objs[1][2]) and np.array_equal(objs[0][3], objs[1][3])
+
+
+KS_KEYS = ("PINS_SPARSE_SWEEP", "PINS_LIST_CAP", "PINS_LIST_MARGIN", "PINS_KSWEEP", "PINS_KSWEEP_START")
+
+
+@pytest.mark.parametrize("name,mk", [("c3s", lambda: make("c3_gmm10k", scale=0.05)),
+                                     ("c4s", lambda: make("c4_l1rect", scale=0.04)),
+                                     ("c1t", lambda: make("c1_rand1k", scale=0.125)),
+                                     ("rag_dense", lambda: ragged(37, 1029, 5)),
+                                     ("c3rs", lambda: make("c3_gmm10k_r", scale=0.03)),
+                                     ("rag_l1_r", lambda: ragged(133, 47, 17, "l1", 3, real=True)),
+                                     ("rag_sq", lambda: ragged(301, 517, 9, "sq", 10))])
+def test_kernel_matrix_sweeps(P, name, mk, monkeypatch):
+    # Absorbed kernel-matrix sweeps (lse_ksweep_kernel, the default of long Sinkhorn phases):
+    # exp(x_ij - r) = K_ij u_j with K fixed since the record pass -- the same sums as the
+    # log-domain pass (Alg. 2 l.5-6) with a different rounding, so f, g agree with the dense
+    # sweeps and with the oracle to the sweep tolerance and the phase stops at the same
+    # sweep.  Settings: from the first sweep on; from sweep 7 (the default); and forced list
+    # overflow (capacity 2: regrowth) with failing certificates (margin 0.01: dense fallback
+    # units and re-records).
+    w = mk()
+    for k in (0, 1):
+        if k == 0:
+            C = po.cost_matrix(w)
+            Ck = po.shifted_cost(C, np.log(w.a)[:, None] + np.log(w.b)[None, :], w.eta)
+            phi, psi, s = w.eta * np.log(w.a), w.eta * np.log(w.b), 1.0
+            f, g = np.zeros(w.m), np.zeros(w.n)
+        else:
+            C, Ck, phi, psi, s, f, g = oracle_state(w, 1)
+            f = f + np.random.default_rng(3).normal(0, 3 * w.eta, w.m)
+        res = []
+        for env in ({"PINS_KSWEEP": "0"}, {"PINS_KSWEEP_START": "0"}, {},
+                    {"PINS_KSWEEP_START": "0", "PINS_LIST_CAP": "2", "PINS_LIST_MARGIN": "0.01"}):
+            for key in KS_KEYS:
+                monkeypatch.delenv(key, raising=False)
+            for key, v in env.items():
+                monkeypatch.setenv(key, v)
+            pb = P.DeviceProblem.from_workload(w)
+            ws = P.Workspace()
+            fd, gd = T(f), T(g)
+            t, r = P.sinkhorn(ws, pb, T(phi), T(psi), s, fd, gd, 0.0, 40)
+            f40, g40 = H(fd).copy(), H(gd).copy()
+            t2, r2 = P.sinkhorn(ws, pb, T(phi), T(psi), s, fd, gd, 1e-3, 400)   # stops on the tolerance
+            res.append((t, r, t2, r2, f40, g40, H(fd), H(gd)))
+        # the oracle's 40 sweeps
+        fo, go = f.copy(), g.copy()
+        for _ in range(40):
+            fo, go = po.sinkhorn_sweep(fo, go, Ck, w.a, w.b, w.eta)
+        scale = max(1.0, s * C.max() / w.eta)
+        tol_f = 1e-13 * scale * w.eta * 41
+        d = res[0]
+        for o in res:
+            assert o[0] == d[0] and o[2] == d[2], (name, k, o[:4], d[:4])
+            assert abs(o[1] - d[1]) <= 1e-9 * abs(d[1]) + 1e-15
+            np.testing.assert_allclose(o[4], fo, rtol=0, atol=tol_f * (1 + np.abs(fo).max() / w.eta))
+            np.testing.assert_allclose(o[5], go, rtol=0, atol=tol_f * (1 + np.abs(go).max() / w.eta))
+            tol2 = 1e-13 * scale * w.eta * (41 + d[2])
+            np.testing.assert_allclose(o[6], d[6], rtol=0, atol=tol2 * (1 + np.abs(d[6]).max() / w.eta))
+            np.testing.assert_allclose(o[7], d[7], rtol=0, atol=tol2 * (1 + np.abs(d[7]).max() / w.eta))
+    # and whole solves
+    objs = []
+    for env in ({"PINS_KSWEEP": "0"}, {"PINS_KSWEEP_START": "0"}):
+        for key in KS_KEYS:
+            monkeypatch.delenv(key, raising=False)
+        for key, v in env.items():
+            monkeypatch.setenv(key, v)
+        pb = P.DeviceProblem.from_workload(w)
+        r = P.solve(pb, P.default_params(K=5, outer_tol=0.0))
+        ph, ps = H(r["phi"]), H(r["psi"])
+        objs.append((r["obj"], r["sweeps"], ph - ph[0], ps + ph[0]))
+    assert objs[0][1] == objs[1][1]
+    # each subproblem is solved to newton_tol, not to rounding: the two runs agree like the
+    # GPU and the oracle traces do (test_solve_trace_matches_oracle: rtol 1e-9)
+    assert abs(objs[0][0] - objs[1][0]) <= 1e-9 * abs(objs[0][0])
+    np.testing.assert_allclose(objs[1][2], objs[0][2], rtol=0, atol=1e-9 * 6)
+    np.testing.assert_allclose(objs[1][3], objs[0][3], rtol=0, atol=1e-9 * 6)
 
 
 @pytest.mark.parametrize("name,scale", [("c4_l1rect", 0.04), ("c3_gmm10k", 0.05), ("c1_rand1k", 0.2)])
