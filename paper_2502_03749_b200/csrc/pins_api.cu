@@ -184,7 +184,7 @@ struct SideBufs {
     // certified candidate lists of the Sinkhorn phase (pins_pass.cuh lse_sparse_kernel)
     DevBuf lcnt, lj, lD, lB, lqref, lqv, lqsv, ldqc, ldqs, lperm, lq;
     // absorbed kernel-matrix sweeps (lse_ksweep_kernel): sliced-ELL copy of the lists
-    DevBuf lqd, lmref, ellj, ellK;
+    DevBuf lqd, ellj, ellK, ellL, ellrel, ellabs, elltot, lunit;
 };
 
 struct pins_workspace {
@@ -711,19 +711,17 @@ cudaError_t launch_lse_sparse(int cost, int dp, int grid, int gfb, int gmerge, s
     return cudaGetLastError();
 }
 
-constexpr size_t kKSmemMax = 200 * 1024;     // lse_ksweep_kernel: the widest split's u_j (8 B per column)
+constexpr size_t kKSmemMax = 220 * 1024;     // lse_ksweep_kernel: the ring + the widest split's u_j (8 B per column)
 
 // the absorbed kernel-matrix path of a half-sweep: ELL build (only right after a record),
 // ELL walk, dense fallback of failed units, merge
 cudaError_t launch_lse_k(int cost, int dp, int grid, int gfb, int gmerge, size_t smem, cudaStream_t st,
                          const PassArgs &A) {
-    const bool f32 = cost == PC_SQTC || cost == PC_SQ32 || cost == PC_L132;
-    if (f32) LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_kbuild_kernel<float><<<grid, kPT, 0, st>>>(A));
-    else LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_kbuild_kernel<double><<<grid, kPT, 0, st>>>(A));
 #define LSK_LAUNCH(C_, DP_)                                                                     \
     do {                                                                                        \
-        LAUNCH(PINS_PROF_KSWEEP, st, lse_ksweep_kernel<C_, DP_><<<grid, kPT,                 \
-               (pass_smem(lse_ksweep_kernel<C_, DP_>, kKSmemMax), smem), st>>>(A));             \
+        LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_kbuild_kernel<C_, DP_><<<grid, kPT, 0, st>>>(A));   \
+        LAUNCH(PINS_PROF_KSWEEP, st, lse_ksweep_kernel<<<grid, kPT,                             \
+               (pass_smem(lse_ksweep_kernel, kKSmemMax), smem), st>>>(A));                      \
         LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_fallback_k_kernel<C_, DP_><<<gfb, kPT, 0, st>>>(A)); \
         LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_merge_kernel<<<gmerge, kPT, 0, st>>>(A));           \
     } while (0)
@@ -768,9 +766,13 @@ int ensure_lists(pins_workspace *ws, const pins_problem *pb, cudaStream_t st, bo
         if (kmode) {
             const long long Mpad = (M + 31) / 32 * 32;
             PINS_TRY(ensure(B.lqd, sizeof(double) * N));
-            PINS_TRY(ensure(B.lmref, sizeof(double) * S * M));
             PINS_TRY(ensure(B.ellj, sizeof(int) * S * ws->lcap * Mpad));
             PINS_TRY(ensure(B.ellK, sizeof(double) * S * ws->lcap * Mpad));
+            PINS_TRY(ensure(B.ellL, sizeof(int) * S * (Mpad / 32)));
+            PINS_TRY(ensure(B.ellrel, sizeof(int) * S * (Mpad / 32)));
+            PINS_TRY(ensure(B.ellabs, sizeof(int) * S * (Mpad / 32)));
+            PINS_TRY(ensure(B.elltot, sizeof(int) * S));
+            PINS_TRY(ensure(B.lunit, 32 * S * Mpad));
         }
     }
     PINS_TRY(ensure(ws->lctl, sizeof(int) * 16));
@@ -821,12 +823,17 @@ int half_sweep(pins_workspace *ws, const pins_problem *pb, int o, const double *
         P.oS = ws->S[1 - o];
         P.lctl = ptr<int>(ws->lctl);
         A.lt = lt;
+        A.lnosort = getenv("PINS_KNOSORT") != nullptr ? 1 : 0;
         A.lmargin = list_margin();
         if (lmode == 2) {
             P.lqd = ptr<double>(B.lqd);
-            P.lmref = ptr<double>(B.lmref);
             P.ellj = ptr<int>(B.ellj);
             P.ellK = ptr<double>(B.ellK);
+            P.ellL = ptr<int>(B.ellL);
+            P.ellrel = ptr<int>(B.ellrel);
+            P.ellabs = ptr<int>(B.ellabs);
+            P.elltot = ptr<int>(B.elltot);
+            P.lunit = B.lunit.p;
             P.Mpad = (P.M + 31) / 32 * 32;
         }
         P.lrec = 1;
@@ -839,7 +846,7 @@ int half_sweep(pins_workspace *ws, const pins_problem *pb, int o, const double *
         const size_t stage = (size_t)wmax * 12 + 16;
         if (lmode == 2) {
             PINS_CUDA(launch_lse_k(cost, ws->dp, (int)(P.S * ((P.M + kPT - 1) / kPT)), 4 * ws->nsm, P.RB,
-                                   (size_t)wmax * 8 + 16, st, A));
+                                   (size_t)wmax * 8 + 16 + kKRing, st, A));
             return PINS_OK;
         }
         P.lstage = stage <= 64 * 1024 ? 1 : 0;
@@ -889,7 +896,7 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
     for (int o = 0; o < 2 && kavail; ++o) {          // the widest split's u_j must fit in shared memory
         const long long N = o == 0 ? pb->n : pb->m, nch = (N + kCC - 1) / kCC;
         const long long wmax = kCC * ((nch + ws->S[o] - 1) / ws->S[o]);
-        if ((size_t)wmax * 8 + 16 > kKSmemMax) kavail = false;
+        if ((size_t)wmax * 8 + 16 + kKRing > kKSmemMax) kavail = false;
     }
     int lmode = 0;
     auto lists_begin = [&](int mode) -> int {
@@ -937,8 +944,9 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
         ws->lstat[3] += hc[4 + 6] + hc[4 + 7];
         if (getenv("PINS_LIST_STATS"))     // dev instrumentation
             fprintf(stderr, "lists: sweeps %d cap %lld max %d overflow %d fallback units %d / %d records %d / %d "
-                    "entries recorded %d / %d\n", hc[1], ws->lcap, hc[4 + 5], hc[4 + 4], hc[4 + 6], hc[4 + 7],
-                    hc[4 + 12], hc[4 + 13], hc[4 + 14], hc[4 + 15]);
+                    "entries recorded %d / %d ELL stages (512 entries) %d / %d\n", hc[1], ws->lcap, hc[4 + 5],
+                    hc[4 + 4], hc[4 + 6], hc[4 + 7], hc[4 + 12], hc[4 + 13], hc[4 + 14], hc[4 + 15], hc[4 + 10],
+                    hc[4 + 11]);
     }
     return PINS_OK;
 }

@@ -170,13 +170,18 @@ struct PassSide {
     int *lq;                        // [S * M] units whose certificate failed (fallback queue)
     int lstage;                     // sparse pass: the split's column values staged in shared memory
     // Absorbed kernel-matrix sweeps (lse_ksweep_kernel): the lists as a sliced-ELL matrix
-    // K_ij = exp(x_ij(record) - lmref) per warp tile of 32 sorted ranks; entry k of lane l of
-    // the tile starting at rank t0 of split sp sits at ((sp * Mpad + t0) * lcap + k * 32 + l
+    // K_ij = exp(x_ij(record) - r_u) per warp tile of 32 sorted ranks, tiles packed densely
+    // in (split, rank) order (a sparse layout would touch every 2 MB page of the arrays)
     double *lqd;                    // [N] the record pass's column values q_j in fp64 (NULL: not kept)
-    double *lmref;                  // [S * M] per unit: the record pass's final reference mx
     int *ellj;                      // [S * Mpad * lcap] column index inside the split (j - jb)
     double *ellK;                   // [S * Mpad * lcap] kernel values
     long long Mpad;                 // M rounded up to whole warp tiles
+    int *ellL;                      // [S * Mpad / 32] k-steps stored per tile (a multiple of kKB)
+    int *ellrel;                    // [S * Mpad / 32] first stage of the tile inside its split's block
+    int *ellabs;                    // [S * Mpad / 32] first stage of the tile (tiles are packed densely:
+                                    // entry k of lane l at (ellabs * kKB + k) * 32 + l)
+    int *elltot;                    // [S] stages per split
+    void *lunit;                    // [S * Mpad] KUnit per sorted rank: what a half-sweep needs of its unit
     // finalize: this side's new potentials are the other side's column values
     double *oqv;                    // [M] q of the other orientation, or NULL
     float *oqsv;                    // [M]
@@ -206,6 +211,7 @@ struct PassArgs {
     int count_sweep;                // LSE col pass: ++ctl[1]
     int test_tol;                   // LSE row pass: set done (and rollback) when res <= tol
     const double *a_dot, *f_dot, *b_dot, *g_dot;   // SUM: <a,f> + <b,g> (global finalize)
+    int lnosort;                    // candidate lists: keep the units in row order (experiments)
     int lt;                         // candidate lists: launch index of this half-sweep
     double lmargin;                 // candidate lists: record margin below the threshold
 };
@@ -931,6 +937,7 @@ __device__ __forceinline__ unsigned phase1(const Buf<COST, DP> &B, const PassSid
 // each pass row in split order, update the potential, residual of the starting
 // iterate, argmax seed; for the candidate lists the new potentials become the other
 // side's column values, with their drift since that side's record pass.
+template <int NB = 8>
 __device__ __forceinline__ void lse_rowblock_finalize(const PassArgs &A, const PassSide &P, int rb, long long i,
                                                       bool valid, const double *thi, const double *tlo, double *red,
                                                       bool *flag, float w_lo, bool rec_ran, bool sparse) {
@@ -938,34 +945,34 @@ __device__ __forceinline__ void lse_rowblock_finalize(const PassArgs &A, const P
     const double inv_eta = A.inv_eta;
     double res = 0.0, dmax = 0.0, dq = -INFINITY;
     if (valid) {
-        // split partials in batches of 8 (independent loads first; the max and the sum
-        // then run in split order, as before)
+        // split partials in batches of NB (independent loads first; the max and the sum
+        // then run in split order, whatever NB)
         double M = -INFINITY;
         int jbest = -1;
-        for (int s0 = 0; s0 < P.S; s0 += 8) {
-            double v[8];
-            int jj[8];
+        for (int s0 = 0; s0 < P.S; s0 += NB) {
+            double v[NB];
+            int jj[NB];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < NB; ++q) {
                 const int s = min(s0 + q, P.S - 1);
                 v[q] = P.pa[(long long)s * P.M + i];
                 jj[q] = P.pj[(long long)s * P.M + i];
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
+            for (int q = 0; q < NB; ++q)
                 if (s0 + q < P.S && v[q] > M) { M = v[q]; jbest = jj[q]; }
         }
         double Ssum = 0.0;
-        for (int s0 = 0; s0 < P.S; s0 += 8) {
-            double v[8], c[8];
+        for (int s0 = 0; s0 < P.S; s0 += NB) {
+            double v[NB], c[NB];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < NB; ++q) {
                 const int s = min(s0 + q, P.S - 1);
                 v[q] = P.pa[(long long)s * P.M + i];
                 c[q] = P.pb[(long long)s * P.M + i];
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
+            for (int q = 0; q < NB; ++q)
                 if (s0 + q < P.S && c[q] > 0.0) Ssum += c[q] * pexp(v[q] - M, thi, tlo);
         }
         const double L = M + log(Ssum);
@@ -1213,6 +1220,12 @@ __global__ void __launch_bounds__(kPT, 5) lse_pass_kernel(PassArgs A, const __gr
 // orders the units by decreasing list length, so the threads of a warp walk lists of
 // about the same length (no divergence) and the long ones start first.
 // =========================================================================
+constexpr int kKB = 16;                 // ELL k-steps per pipeline stage (32 lanes x kKB entries)
+constexpr int kKNS = 2;                 // stages per warp
+constexpr int kKStJ = kKB * 32 * 4;     // stage bytes: columns (int32)
+constexpr int kKStK = kKB * 32 * 8;     // stage bytes: kernel values (fp64)
+constexpr int kKRing = (kPT / 32) * kKNS * (kKStJ + kKStK);   // 96 KB per CTA
+
 // per split, the pass rows by decreasing list length (counting sort in 64 length
 // buckets, one CTA per split); only right after a record
 __global__ void __launch_bounds__(1024) lse_sort_kernel(PassArgs A) {
@@ -1222,20 +1235,53 @@ __global__ void __launch_bounds__(1024) lse_sort_kernel(PassArgs A) {
     const int sp = blockIdx.x, tid = threadIdx.x;
     const int *cnt = P.lcnt + (long long)sp * P.M;
     int *perm = P.lperm + (long long)sp * P.M;
-    if (tid < 64) hist[tid] = 0;
+    if (A.lnosort) {
+        for (long long i = tid; i < P.M; i += 1024) perm[i] = (int)i;
+    } else {
+        if (tid < 64) hist[tid] = 0;
+        __syncthreads();
+        auto key = [&](long long i) {
+            const int c = cnt[i];
+            return c < 0 ? 0 : 63 - min(63, c >> 3);           // descending length; overflow first
+        };
+        for (long long i = tid; i < P.M; i += 1024) atomicAdd(hist + key(i), 1);
+        __syncthreads();
+        if (tid == 0) {
+            int acc = 0;
+            for (int k = 0; k < 64; ++k) { const int h = hist[k]; hist[k] = acc; acc += h; }
+        }
+        __syncthreads();
+        for (long long i = tid; i < P.M; i += 1024) perm[atomicAdd(hist + key(i), 1)] = (int)i;
+    }
+    if (!P.ellL) return;
+    // kernel-matrix mode: the ELL tile (32 consecutive ranks) lengths in whole stages of kKB
+    // k-steps, and their dense packing offsets inside the split
     __syncthreads();
-    auto key = [&](long long i) {
-        const int c = cnt[i];
-        return c < 0 ? 0 : 63 - min(63, c >> 3);           // descending length; overflow first
-    };
-    for (long long i = tid; i < P.M; i += 1024) atomicAdd(hist + key(i), 1);
-    __syncthreads();
-    if (tid == 0) {
-        int acc = 0;
-        for (int k = 0; k < 64; ++k) { const int h = hist[k]; hist[k] = acc; acc += h; }
+    const int ntile = (int)(P.Mpad / 32), lane = tid & 31, warp = tid >> 5;
+    int *tl = P.ellL + (long long)sp * ntile, *to = P.ellrel + (long long)sp * ntile;
+    for (int tt = warp; tt < ntile; tt += 32) {
+        const long long r = (long long)tt * 32 + lane;
+        const int c = r < P.M ? max(0, cnt[perm[r]]) : 0;
+        const int L = (__reduce_max_sync(0xffffffffu, c) + kKB - 1) / kKB * kKB;
+        if (lane == 0) tl[tt] = L;
     }
     __syncthreads();
-    for (long long i = tid; i < P.M; i += 1024) perm[atomicAdd(hist + key(i), 1)] = (int)i;
+    if (warp == 0) {
+        int run = 0;
+        for (int t0 = 0; t0 < ntile; t0 += 32) {
+            const int tt = t0 + lane;
+            const int v = tt < ntile ? tl[tt] / kKB : 0;
+            int inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int nb = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += nb;
+            }
+            if (tt < ntile) to[tt] = run + inc - v;
+            run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) P.elltot[sp] = run;
+    }
 }
 
 template <int COST, int DP, bool STG>
@@ -1520,7 +1566,7 @@ __global__ void __launch_bounds__(kPT) lse_merge_kernel(PassArgs A) {
     const int rb = blockIdx.x;
     const long long i = (long long)rb * kPT + threadIdx.x;
     const float w_lo = (float)A.w * (1.f - 0x1p-19f);
-    lse_rowblock_finalize(A, P, rb, i, i < P.M, thi, tlo, red, &flag, w_lo, false, true);
+    lse_rowblock_finalize<32>(A, P, rb, i, i < P.M, thi, tlo, red, &flag, w_lo, false, true);
 }
 
 // =========================================================================
@@ -1542,10 +1588,26 @@ __global__ void __launch_bounds__(kPT) lse_merge_kernel(PassArgs A) {
 // every term carries a few ulps of relative error instead of the error of x - mx
 // (DESIGN.md section 5).
 // =========================================================================
-constexpr int kKB = 16;                 // ELL entries per lane in flight (loads of one batch)
+// 1D bulk copy global -> shared by the TMA unit (SASS UBLKCP), completion on an mbarrier
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        ::"r"(tc::smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(tc::smem_u32(mbar))
+        : "memory");
+}
 
-template <class DT>
+// per sorted rank: the unit's row, list length, certificate data (list bound lB, argmax seed
+// column js with its distance -- the seed stays put between records: kernel-matrix passes
+// leave jstar alone) and reference, one 32-byte record read by every half-sweep
+struct __align__(16) KUnit {
+    int i, cnt, js;
+    float lB;
+    double Dseed, mref;
+};
+
+template <int COST, int DP>
 __global__ void __launch_bounds__(kPT) lse_kbuild_kernel(PassArgs A) {
+    using DT = LDT<COST>;
     __shared__ double thi[64], tlo[64];
     const PassSide &P = A.side[0];
     if (P.lctl[2 + P.lori] != A.lt) return;          // only right after a record
@@ -1564,11 +1626,35 @@ __global__ void __launch_bounds__(kPT) lse_kbuild_kernel(PassArgs A) {
         u = (long long)sp * P.M + i;
         cnt = max(0, P.lcnt[u]);
         mref = P.pa[u];                              // the record pass's reference of this unit
-        P.lmref[u] = mref;
+        KUnit un;
+        un.i = (int)i;
+        un.cnt = P.lcnt[u];
+        un.js = P.jstar[i];
+        un.lB = P.lB[i];
+        un.Dseed = 0.0;
+        if (un.js >= 0 && un.js < P.N) {
+            RowPt<COST, DP> rp;
+            rp.load(P, i, true);
+            un.Dseed = dist_global<COST, DP>(P, rp, i, un.js);
+        } else {
+            un.js = -1;
+        }
+        un.mref = mref;
+        reinterpret_cast<KUnit *>(P.lunit)[(long long)sp * P.Mpad + t] = un;
     }
-    // the tile is zero-padded to whole batches of kKB list entries (lcap is a multiple of kKB)
-    const int L = (__reduce_max_sync(0xffffffffu, cnt) + kKB - 1) / kKB * kKB;
-    const long long base = ((long long)sp * P.Mpad + (t & ~31LL)) * P.lcap + lane;
+    // the tile is zero-padded to whole stages of kKB k-steps (lse_sort_kernel: lengths and
+    // packing offsets)
+    const bool tile = (t & ~31LL) < P.M;
+    const long long te = (long long)sp * (P.Mpad / 32) + (t >> 5);
+    int sbase = 0;
+    for (int q = 0; q < sp; ++q) sbase += P.elltot[q];
+    const int L = tile ? P.ellL[te] : 0;
+    const int tabs = tile ? sbase + P.ellrel[te] : 0;
+    const long long base = (long long)tabs * (kKB * 32) + lane;
+    if (lane == 0 && tile) {
+        P.ellabs[te] = tabs;
+        atomicAdd(P.lctl + 10 + P.lori, L / kKB);       // stats: stages stored (512 entries each)
+    }
     const DT *lD = reinterpret_cast<const DT *>(P.lD) + u * P.lcap;
     const int *lj = P.lj + u * P.lcap;
     const double w = A.w;
@@ -1586,80 +1672,99 @@ __global__ void __launch_bounds__(kPT) lse_kbuild_kernel(PassArgs A) {
     }
 }
 
-template <int COST, int DP>
 __global__ void __launch_bounds__(kPT) lse_ksweep_kernel(PassArgs A) {
-    extern __shared__ __align__(16) unsigned char lsm[];   // u_j of the split's columns
+    // dynamic shared memory: the ring (per warp kKNS stages of kKB k-steps), then u_j of
+    // the split's columns
+    extern __shared__ __align__(128) unsigned char lsm[];
     __shared__ double thi[64], tlo[64];
+    __shared__ uint64_t kbar[kPT / 32][kKNS];
     if (A.check_done && A.ctl[0]) return;            // Sinkhorn phase already converged
     const PassSide &P = A.side[0];
     if (P.lctl[2 + P.lori] == A.lt) return;          // the dense pass recorded this half-sweep
-    const int sp = blockIdx.x % P.S, lane = threadIdx.x & 31;
+    const int sp = blockIdx.x % P.S, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long t = (long long)(blockIdx.x / P.S) * kPT + threadIdx.x;
     long long jb, je;
     split_range(P.N, P.S, sp, jb, je);
     load_exp_table(A.tab, thi, tlo);
+    // The warp's tile is one contiguous block of L x 32 entries per array: stages of kKB
+    // k-steps are brought into the warp's ring by 1D bulk copies (lane 0 issues, the TMA
+    // unit completes on the stage's mbarrier), kKNS stages in flight -- memory-level
+    // parallelism without registers.  The first stages are issued before anything else,
+    // so the certificate and the column factors below overlap their latency.
+    const bool tile = (t & ~31LL) < P.M;
+    const long long te = (long long)sp * (P.Mpad / 32) + (t >> 5);
+    const long long tile0 = tile ? (long long)P.ellabs[te] * (kKB * 32) : 0;
+    unsigned char *ring = lsm + warp * (kKNS * (kKStJ + kKStK));
+    uint64_t *bar = kbar[warp];
+    const int nb = tile ? P.ellL[te] / kKB : 0;
+    auto issue = [&](int b) {
+        const int st = b % kKNS;
+        unsigned char *dst = ring + st * (kKStJ + kKStK);
+        mbar_expect_tx(&bar[st], kKStJ + kKStK);
+        bulk_load(dst, P.ellK + tile0 + (long long)b * (kKB * 32), kKStK, &bar[st]);
+        bulk_load(dst + kKStK, P.ellj + tile0 + (long long)b * (kKB * 32), kKStJ, &bar[st]);
+    };
+    if (lane == 0) {
+        for (int st = 0; st < kKNS; ++st) tc::mbar_init(&kbar[warp][st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        for (int b = 0; b < min(nb, kKNS); ++b) issue(b);
+    }
+    KUnit kun;
+    kun.i = 0; kun.cnt = 0; kun.js = -1; kun.lB = 0.f; kun.Dseed = 0.0; kun.mref = 0.0;
+    if (t < P.M) kun = reinterpret_cast<const KUnit *>(P.lunit)[(long long)sp * P.Mpad + t];
+    const double qseed = kun.js >= 0 ? __ldg(P.lqv + kun.js) : 0.0;
     __syncthreads();
     const float dq = P.ldqs[sp];
     const double shift = (dq == dq && fabsf(dq) != INFINITY) ? (double)dq : 0.0;
-    double *su = reinterpret_cast<double *>(lsm);
+    double *su = reinterpret_cast<double *>(lsm + kKRing);
     for (long long j = jb + threadIdx.x; j < je; j += kPT) {
         const double q = __ldg(P.lqv + j), qr = __ldg(P.lqd + j);
         su[j - jb] = (q == -INFINITY || qr == -INFINITY) ? 0.0 : pexp(q - qr - shift, thi, tlo);
     }
     __syncthreads();
-    const bool act = t < P.M;
-    long long i = 0, u = 0;
+    long long u = 0;
     int cnt = 0;
+    double mref = 0.0;
     bool ok = false;
-    if (act) {
-        i = P.lperm[(long long)sp * P.M + t];
-        u = (long long)sp * P.M + i;
-        cnt = P.lcnt[u];
+    if (t < P.M) {
+        const KUnit un = kun;
+        u = (long long)sp * P.M + un.i;
+        cnt = un.cnt;
+        mref = un.mref;
         // the unit certificate of lse_sparse_kernel: no unlisted entry can pass the LSE cut
-        RowPt<COST, DP> rp;
-        rp.load(P, i, true);
-        double mx = -INFINITY;
-        const int js = P.jstar[i];
-        if (js >= 0 && js < P.N) mx = fma(-A.w, dist_global<COST, DP>(P, rp, i, js), P.lqv[js]);
+        const double mx = un.js >= 0 ? fma(-A.w, un.Dseed, qseed) : -INFINITY;
         const float thr0 = thr_lo_of(mx - kLseCut);
-        const float B = P.lB[i];
+        const float B = un.lB;
         const double ub = (double)B + (double)ulpf_of(B) + (double)dq;
         ok = cnt >= 0 && thr0 != -INFINITY && dq != INFINITY &&
              ub + 1e-12 * (fabs((double)B) + fabs((double)dq)) <= (double)thr0;
         if (!ok) P.lq[atomicAdd(P.lctl + 8, 1)] = (int)u;     // dense scan (fallback kernel)
     }
-    const int L = __reduce_max_sync(0xffffffffu, ok ? cnt : 0);
-    const long long base = ((long long)sp * P.Mpad + (t & ~31LL)) * P.lcap + lane;
-    const int *ej = P.ellj + base;
-    const double *eK = P.ellK + base;
-    // lanes past their own list read the tile's zero padding (K = 0, column 0).  Whole
-    // batches of kKB entries per lane: the loads of a batch are independent and all in
-    // flight together (the longest tiles are a serial chain of L / kKB memory latencies)
+    // lanes past their own list read the tile's zero padding (K = 0, column 0)
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    for (int k = 0; k < L; k += kKB) {
-        int jj[kKB];
-        double KK[kKB];
-#pragma unroll
-        for (int q = 0; q < kKB; ++q) {
-            jj[q] = __ldcs(ej + (k + q) * 32);
-            KK[q] = __ldcs(eK + (k + q) * 32);
-        }
+    for (int b = 0; b < nb; ++b) {
+        const int st = b % kKNS;
+        tc::mbar_wait(&bar[st], (uint32_t)((b / kKNS) & 1));
+        const double *sK = reinterpret_cast<const double *>(ring + st * (kKStJ + kKStK)) + lane;
+        const int *sj = reinterpret_cast<const int *>(ring + st * (kKStJ + kKStK) + kKStK) + lane;
 #pragma unroll
         for (int q = 0; q < kKB; q += 4) {
-            s0 = fma(KK[q + 0], su[jj[q + 0]], s0);
-            s1 = fma(KK[q + 1], su[jj[q + 1]], s1);
-            s2 = fma(KK[q + 2], su[jj[q + 2]], s2);
-            s3 = fma(KK[q + 3], su[jj[q + 3]], s3);
+            s0 = fma(sK[(q + 0) * 32], su[sj[(q + 0) * 32]], s0);
+            s1 = fma(sK[(q + 1) * 32], su[sj[(q + 1) * 32]], s1);
+            s2 = fma(sK[(q + 2) * 32], su[sj[(q + 2) * 32]], s2);
+            s3 = fma(sK[(q + 3) * 32], su[sj[(q + 3) * 32]], s3);
         }
+        __syncwarp();                                // every lane is done with this stage
+        if (lane == 0 && b + kKNS < nb) issue(b + kKNS);
     }
+    count_survivors(A.count_surv, 2, ok && cnt > 0 ? cnt : 0);       // ELL entries walked (profiling)
     if (!ok) return;
     const double sm = (s0 + s1) + (s2 + s3);
     if (cnt > 0 && !(sm > 1e-280)) {                 // every listed term underflowed: exact dense scan
         P.lq[atomicAdd(P.lctl + 8, 1)] = (int)u;
         return;
     }
-    if (A.count_surv && cnt) atomicAdd(g_surv + 2, (unsigned long long)cnt);   // ELL entries walked
-    P.pa[u] = cnt > 0 ? P.lmref[u] + shift : -INFINITY;
+    P.pa[u] = cnt > 0 ? mref + shift : -INFINITY;
     P.pb[u] = sm;
     P.pj[u] = -1;
 }
@@ -1690,14 +1795,22 @@ __global__ void __launch_bounds__(kPT) lse_fallback_k_kernel(PassArgs A) {
         RowPt<COST, DP> rp;
         rp.load(P, i, true);
         double mx = -INFINITY, sm = 0.0;
-        for (long long j = jb + lane; j < je; j += 32) {
-            const double x = fma(-w, dist_global<COST, DP>(P, rp, i, j), __ldg(P.lqv + j));
-            if (x == -INFINITY) continue;
-            if (x > mx) {
-                sm = fma(sm, pexp(mx - x, thi, tlo), 1.0);
-                mx = x;
-            } else {
-                sm += pexp(x - mx, thi, tlo);
+        for (long long j0 = jb + lane; j0 < je; j0 += 128) {      // 4 columns per lane and step: loads first
+            double x[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const long long j = j0 + 32 * q;
+                x[q] = j < je ? fma(-w, dist_global<COST, DP>(P, rp, i, j), __ldg(P.lqv + j)) : -INFINITY;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (x[q] == -INFINITY) continue;
+                if (x[q] > mx) {
+                    sm = fma(sm, pexp(mx - x[q], thi, tlo), 1.0);
+                    mx = x[q];
+                } else {
+                    sm += pexp(x[q] - mx, thi, tlo);
+                }
             }
         }
         const double Mx = warp_max(mx);
