@@ -716,10 +716,11 @@ constexpr size_t kKSmemMax = 220 * 1024;     // lse_ksweep_kernel: the ring + th
 // the absorbed kernel-matrix path of a half-sweep: ELL build (only right after a record),
 // ELL walk, dense fallback of failed units, merge
 cudaError_t launch_lse_k(int cost, int dp, int grid, int gfb, int gmerge, size_t smem, cudaStream_t st,
-                         const PassArgs &A) {
+                         const PassArgs &A, bool build) {
 #define LSK_LAUNCH(C_, DP_)                                                                     \
     do {                                                                                        \
-        LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_kbuild_kernel<C_, DP_><<<grid, kPT, 0, st>>>(A));   \
+        if (build)                                                                              \
+            LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_kbuild_kernel<C_, DP_><<<grid, kPT, 0, st>>>(A)); \
         LAUNCH(PINS_PROF_KSWEEP, st, lse_ksweep_kernel<<<grid, kPT,                             \
                (pass_smem(lse_ksweep_kernel, kKSmemMax), smem), st>>>(A));                      \
         LAUNCH(PINS_PROF_SWEEP_AUX, st, lse_fallback_k_kernel<C_, DP_><<<gfb, kPT, 0, st>>>(A)); \
@@ -786,7 +787,10 @@ int ensure_lists(pins_workspace *ws, const pins_problem *pb, cudaStream_t st, bo
 // this half-sweep's launch index).
 int half_sweep(pins_workspace *ws, const pins_problem *pb, int o, const double *phi, const double *psi,
                double s, double *f, double *g, bool check_done, bool test_tol, cudaStream_t st,
-               int lmode = 0, int lt = 0) {
+               int lmode = 0, int lt = 0, bool rec_now = true) {
+    // rec_now (mode 2): queue the record pass, sort and ELL build of this half-sweep (the host
+    // saw the side's re-record request at its last synchronisation); otherwise only the ELL
+    // walk, the fallback scan and the merge are launched
     PassArgs A;
     base_args(ws, pb, s, A);
     fill_side(ws, pb, o, f, phi, g, psi, A.side[0]);
@@ -836,17 +840,20 @@ int half_sweep(pins_workspace *ws, const pins_problem *pb, int o, const double *
             P.lunit = B.lunit.p;
             P.Mpad = (P.M + 31) / 32 * 32;
         }
-        P.lrec = 1;
-        PINS_CUDA(launch_lse(cost, ws->dp, A.G0, st, A, o == 0 ? ws->tm_row : ws->tm_col,
-                             lmode == 2 ? PINS_PROF_SWEEP_AUX : -1));
-        P.lrec = 0;
-        LAUNCH(lmode == 2 ? PINS_PROF_SWEEP_AUX : PINS_PROF_SWEEP_ROW, st, lse_sort_kernel<<<P.S, 1024, 0, st>>>(A));
+        if (lmode != 2 || rec_now) {
+            P.lrec = 1;
+            PINS_CUDA(launch_lse(cost, ws->dp, A.G0, st, A, o == 0 ? ws->tm_row : ws->tm_col,
+                                 lmode == 2 ? PINS_PROF_SWEEP_AUX : -1));
+            P.lrec = 0;
+            LAUNCH(lmode == 2 ? PINS_PROF_SWEEP_AUX : PINS_PROF_SWEEP_ROW, st,
+                   lse_sort_kernel<<<P.S, 1024, 0, st>>>(A));
+        }
         // the widest split's column values (q fp64 + qs fp32) staged per CTA when they fit
         const long long nch = (P.N + kCC - 1) / kCC, wmax = kCC * ((nch + P.S - 1) / P.S);
         const size_t stage = (size_t)wmax * 12 + 16;
         if (lmode == 2) {
             PINS_CUDA(launch_lse_k(cost, ws->dp, (int)(P.S * ((P.M + kPT - 1) / kPT)), 4 * ws->nsm, P.RB,
-                                   (size_t)wmax * 8 + 16 + kKRing, st, A));
+                                   (size_t)wmax * 8 + 16 + kKRing, st, A, rec_now));
             return PINS_OK;
         }
         P.lstage = stage <= 64 * 1024 ? 1 : 0;
@@ -911,13 +918,29 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
     if (walk) PINS_TRY(lists_begin(1));
     int done = 0, batch = 1, queued = 0, lt = 0;
     int *hc = reinterpret_cast<int *>(ws->h + 40);
+    // Mode 2 is driven in short batches (8 sweeps).  The device raises a side's re-record
+    // request when more than 2 % of its units fail their certificate; the host reads the
+    // requests at every synchronisation and queues the record pass, the sort and the ELL build
+    // only in the first sweep of the next batch (failed units are scanned densely meanwhile),
+    // so an ordinary half-sweep is three launches: ELL walk, fallback scan, merge.
+    // Churn control: while the potentials still move fast (the first sweeps of a cold start)
+    // certificates fail within a sweep or two of a record.  A batch in which more than 1/8 of
+    // the unit passes fell back sends the phase to dense sweeps for `cool` sweeps (doubling).
+    int cool = 0, cool_len = 32;
+    long long fb_prev = 0;
+    bool need[2] = {true, true};
+    const long long units = (long long)ws->S[0] * pb->m + (long long)ws->S[1] * pb->n;
     while (!done && queued < prm->T1) {
-        if (kavail && lmode == 0 && queued >= kstart) PINS_TRY(lists_begin(2));
-        const int nb = std::min(batch, prm->T1 - queued);
+        if (kavail && lmode == 0 && queued >= kstart && cool <= 0) {
+            PINS_TRY(lists_begin(2));
+            fb_prev = 0;
+            need[0] = need[1] = true;
+        }
+        const int nb = std::min(lmode == 2 ? std::min(batch, 8) : batch, prm->T1 - queued);
         for (int q = 0; q < nb; ++q) {
             const bool first = (queued + q) == 0;
-            PINS_TRY(half_sweep(ws, pb, 0, phi, psi, s, f, g, true, !first, st, lmode, lt++));
-            PINS_TRY(half_sweep(ws, pb, 1, phi, psi, s, f, g, true, false, st, lmode, lt++));
+            PINS_TRY(half_sweep(ws, pb, 0, phi, psi, s, f, g, true, !first, st, lmode, lt++, q == 0 && need[0]));
+            PINS_TRY(half_sweep(ws, pb, 1, phi, psi, s, f, g, true, false, st, lmode, lt++, q == 0 && need[1]));
         }
         queued += nb;
         PINS_CUDA(cudaMemcpyAsync(hc, ws->ctl.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
@@ -929,6 +952,22 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
             PINS_CUDA(cudaMemcpyAsync(f, ws->fsave.p, sizeof(double) * pb->m, cudaMemcpyDeviceToDevice, st));
         }
         batch = std::min(batch * 2, 64);
+        if (lmode == 0 && cool > 0) cool -= nb;
+        if (lmode == 2) {
+            need[0] = hc[4 + 0] != 0;
+            need[1] = hc[4 + 1] != 0;
+        }
+        if (lmode == 2 && !done && hc[4 + 4] == 0) {
+            const long long fb = (long long)hc[4 + 6] + hc[4 + 7];
+            const long long dfb = fb - fb_prev;
+            fb_prev = fb;
+            if (dfb * 8 > units * nb && !getenv("PINS_KSWEEP_NOCOOL")) {
+                lmode = 0;
+                cool = cool_len;
+                cool_len = std::min(2 * cool_len, 512);
+                ++ws->lstat[1];
+            }
+        }
         if (lmode && !done && hc[4 + 4] > 0) {
             // a list past capacity (its (split, row) scans densely): grow the lists (the
             // stream is idle here) and record them again
@@ -937,6 +976,7 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
             const int init[14] = {1, 1, -1, -1, 0, 0, hc[4 + 6], hc[4 + 7], 0, 0, 0, 0, hc[4 + 12], hc[4 + 13]};
             PINS_CUDA(cudaMemcpyAsync(ws->lctl.p, init, sizeof init, cudaMemcpyHostToDevice, st));
             ++ws->lstat[2];
+            need[0] = need[1] = true;
         }
     }
     const bool lists = lmode != 0;

@@ -1795,15 +1795,15 @@ __global__ void __launch_bounds__(kPT) lse_fallback_k_kernel(PassArgs A) {
         RowPt<COST, DP> rp;
         rp.load(P, i, true);
         double mx = -INFINITY, sm = 0.0;
-        for (long long j0 = jb + lane; j0 < je; j0 += 128) {      // 4 columns per lane and step: loads first
-            double x[4];
+        for (long long j0 = jb + lane; j0 < je; j0 += 256) {      // 8 columns per lane and step: loads first
+            double x[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < 8; ++q) {
                 const long long j = j0 + 32 * q;
                 x[q] = j < je ? fma(-w, dist_global<COST, DP>(P, rp, i, j), __ldg(P.lqv + j)) : -INFINITY;
             }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < 8; ++q) {
                 if (x[q] == -INFINITY) continue;
                 if (x[q] > mx) {
                     sm = fma(sm, pexp(mx - x[q], thi, tlo), 1.0);

@@ -656,7 +656,8 @@ def test_sparse_sweeps_bit_identical(P, name, mk, monkeypatch):
     assert np.array_equal(objs[0][2], objs[1][2]) and np.array_equal(objs[0][3], objs[1][3])
 
 
-KS_KEYS = ("PINS_SPARSE_SWEEP", "PINS_LIST_CAP", "PINS_LIST_MARGIN", "PINS_KSWEEP", "PINS_KSWEEP_START")
+KS_KEYS = ("PINS_SPARSE_SWEEP", "PINS_LIST_CAP", "PINS_LIST_MARGIN", "PINS_KSWEEP", "PINS_KSWEEP_START",
+           "PINS_KSWEEP_NOCOOL")
 
 
 @pytest.mark.parametrize("name,mk", [("c3s", lambda: make("c3_gmm10k", scale=0.05)),
@@ -671,9 +672,10 @@ def test_kernel_matrix_sweeps(P, name, mk, monkeypatch):
     # exp(x_ij - r) = K_ij u_j with K fixed since the record pass -- the same sums as the
     # log-domain pass (Alg. 2 l.5-6) with a different rounding, so f, g agree with the dense
     # sweeps and with the oracle to the sweep tolerance and the phase stops at the same
-    # sweep.  Settings: from the first sweep on; from sweep 7 (the default); and forced list
-    # overflow (capacity 2: regrowth) with failing certificates (margin 0.01: dense fallback
-    # units and re-records).
+    # sweep.  Settings: from the first sweep on; from sweep 7 (the default); without the
+    # churn control (the phase stays in kernel-matrix mode however many units fall back);
+    # and forced list overflow (capacity 2: regrowth) with failing certificates (margin
+    # 0.01: dense fallback units and re-records).
     w = mk()
     for k in (0, 1):
         if k == 0:
@@ -686,7 +688,9 @@ def test_kernel_matrix_sweeps(P, name, mk, monkeypatch):
             f = f + np.random.default_rng(3).normal(0, 3 * w.eta, w.m)
         res = []
         for env in ({"PINS_KSWEEP": "0"}, {"PINS_KSWEEP_START": "0"}, {},
-                    {"PINS_KSWEEP_START": "0", "PINS_LIST_CAP": "2", "PINS_LIST_MARGIN": "0.01"}):
+                    {"PINS_KSWEEP_START": "0", "PINS_KSWEEP_NOCOOL": "1"},
+                    {"PINS_KSWEEP_START": "0", "PINS_LIST_CAP": "2", "PINS_LIST_MARGIN": "0.01",
+                     "PINS_KSWEEP_NOCOOL": "1"}):
             for key in KS_KEYS:
                 monkeypatch.delenv(key, raising=False)
             for key, v in env.items():

@@ -12,6 +12,9 @@ cap() {   # tag mode regex skip
   if [ -n "$5" ]; then ncu -i /tmp/prof_$tag.ncu-rep --page source --csv --print-source sass 2>&1 | gzip > gpurun_out/ncu_r2_${tag}_src_sass.csv.gz; fi
 }
 cap sweep sweep 'lse_pass' 40 src
+cap ksweep ksweep 'lse_ksweep' 400 src
+cap ksmerge ksweep 'lse_merge' 400
+cap ksfallback ksweep 'lse_fallback_k' 400
 cap eval eval 'sum_pass' 5
 cap denserow dense 'lse_pass_kernel<\(int\)7' 6
 cap densecol dense 'lse_pass_kernel<\(int\)8' 6

@@ -1,6 +1,6 @@
 """Short, deterministic targets for `ncu --set full` (one kernel family per mode).
 
-    python tools/ncu_target.py sweep|eval|cg|late|dense|spmv [config]
+    python tools/ncu_target.py sweep|eval|cg|late|dense|spmv|ksweep [config]
 sweep: 30 Sinkhorn sweeps from X^0 in one device-side phase (lse_pass_kernel);
 eval: 20 sweeps then 10 evaluations with sparsify (sum_pass_kernel); cg: a PINS
 solve capped at 10 outer iterations; late: a PINS solve capped at 300 outer
@@ -18,7 +18,18 @@ from workloads import make
 mode = sys.argv[1]
 name = sys.argv[2] if len(sys.argv) > 2 else "c3_gmm10k"
 w = make(name)
-if mode in ("sweep", "eval"):
+if mode != "ksweep":
+    os.environ["PINS_KSWEEP"] = "0"      # the dense passes themselves (long phases default to kernel-matrix sweeps)
+if mode == "ksweep":
+    # 600 sweeps of one phase from X^0: dense sweeps while the potentials churn, then
+    # absorbed kernel-matrix sweeps (lse_ksweep_kernel + fallback + merge)
+    pb = pins.DeviceProblem.from_workload(w)
+    phi, psi, s = pins.center_init(pb)
+    f = torch.zeros(w.m, dtype=torch.float64, device="cuda")
+    g = torch.zeros(w.n, dtype=torch.float64, device="cuda")
+    ws = pins.Workspace()
+    pins.sinkhorn(ws, pb, phi, psi, s, f, g, 0.0, 600)
+elif mode in ("sweep", "eval"):
     pb = pins.DeviceProblem.from_workload(w)
     phi, psi, s = pins.center_init(pb)
     f = torch.zeros(w.m, dtype=torch.float64, device="cuda")
