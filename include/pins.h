@@ -122,6 +122,15 @@ int pins_sinkhorn_sweep(pins_workspace *ws, const pins_problem *pb, const double
  * pins_sinkhorn_sweep until ||grad P^k||_1 <= tol or max_sweeps sweeps; stops
  * at exactly the first iterate whose residual is <= tol (the test runs on
  * the device; batches of sweeps are queued without host round trips).
+ * A phase longer than 7 sweeps continues with absorbed kernel-matrix sweeps
+ * (DESIGN.md section 5): inside one phase only the column potentials move, so
+ * exp(x_ij - r_i) = K_ij u_j with K fixed since the last record pass; a
+ * half-sweep is then one exponential per column and one FMA per listed entry
+ * of a sliced-ELL copy of K (entries within the log-sum-exp cut of the row
+ * maximum, plus a margin; a per-(row, split) certificate proves that unlisted
+ * entries stay below the cut, failed units are scanned densely).  Same sums as
+ * the log-domain sweep up to rounding (tested against the oracle and against
+ * the dense sweeps); environment PINS_KSWEEP=0 keeps every sweep dense.
  * *sweeps_host = sweeps done, *res_host = final ||grad P^k||_1.  Synchronises. */
 int pins_sinkhorn(pins_workspace *ws, const pins_problem *pb, const double *phi, const double *psi,
                   double s, double *f, double *g, double tol, int32_t max_sweeps, int32_t *sweeps_host,
