@@ -1025,7 +1025,7 @@ __device__ __forceinline__ void lse_rowblock_finalize(const PassArgs &A, const P
         A.st[0] = R;
         A.st[1] = DM;
         if (A.count_sweep) A.ctl[1] += 1;
-        skip_switch(P, w_lo);
+        if (!sparse) skip_switch(P, w_lo);    // list passes stream no chunks: the skip period is not theirs
         if (rec_ran) {                        // lists recorded: the sparse path of this half-sweep exits
             P.lctl[P.lori] = 0;
             P.lctl[2 + P.lori] = A.lt;
