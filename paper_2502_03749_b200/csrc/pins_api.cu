@@ -906,9 +906,42 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
         if ((size_t)wmax * 8 + 16 + kKRing > kKSmemMax) kavail = false;
     }
     int lmode = 0;
+    // device bytes of both sides' lists (and ELL copies) at capacity cap per (row, split); the
+    // capacity is a worst case -- the ELL tiles are packed, most of it is never touched -- but
+    // it is allocated, so list modes are declined when it would not fit comfortably
+    auto list_bytes = [&](long long cap, bool kmode) -> double {
+        double tot = 0.0;
+        for (int o = 0; o < 2; ++o) {
+            const double M = (double)(o == 0 ? pb->m : pb->n), S = (double)ws->S[o];
+            tot += S * M * (double)cap * (kmode ? 12.0 + 12.0 : 12.0);
+        }
+        return tot;
+    };
+    auto list_budget = [&]() -> double {
+        size_t fr = 0, tt = 0;
+        if (cudaMemGetInfo(&fr, &tt) != cudaSuccess) return 0.0;
+        double have = 0.0;      // what the workspace already holds of these buffers is reusable
+        for (int o = 0; o < 2; ++o)
+            have += (double)(ws->sb[o].lj.bytes + ws->sb[o].lD.bytes + ws->sb[o].ellj.bytes + ws->sb[o].ellK.bytes);
+        return std::min(32e9, 0.5 * ((double)fr + have));
+    };
     auto lists_begin = [&](int mode) -> int {
-        if (ws->lcap == 0) ws->lcap = getenv("PINS_LIST_CAP") ? std::max(1LL, atoll(getenv("PINS_LIST_CAP"))) : 64;
+        if (ws->lcap == 0) {
+            // a unit cannot list more than its split's columns: start there (capped), so the
+            // usual instance never regrows
+            long long wmx = 0;
+            for (int o = 0; o < 2; ++o) {
+                const long long N = o == 0 ? pb->n : pb->m, nch = (N + kCC - 1) / kCC;
+                wmx = std::max(wmx, kCC * ((nch + ws->S[o] - 1) / ws->S[o]));
+            }
+            ws->lcap = getenv("PINS_LIST_CAP") ? std::max(1LL, atoll(getenv("PINS_LIST_CAP")))
+                                               : std::max(64LL, std::min(wmx, 512LL));
+        }
         ws->lcap = (ws->lcap + 15) / 16 * 16;     // lists padded to whole batches (8 walk, 16 ELL)
+        if (mode == 2 && list_bytes(ws->lcap, true) > list_budget()) {
+            kavail = false;                        // too large for this device: dense sweeps
+            return PINS_OK;
+        }
         PINS_TRY(ensure_lists(ws, pb, st, mode == 2));
         const int init[16] = {1, 1, -1, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         PINS_CUDA(cudaMemcpyAsync(ws->lctl.p, init, sizeof init, cudaMemcpyHostToDevice, st));
@@ -932,7 +965,7 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
     const long long units = (long long)ws->S[0] * pb->m + (long long)ws->S[1] * pb->n;
     while (!done && queued < prm->T1) {
         if (kavail && lmode == 0 && queued >= kstart && cool <= 0) {
-            PINS_TRY(lists_begin(2));
+            PINS_TRY(lists_begin(2));                // (declines when the lists would not fit)
             fb_prev = 0;
             need[0] = need[1] = true;
         }
@@ -971,7 +1004,14 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
         if (lmode && !done && hc[4 + 4] > 0) {
             // a list past capacity (its (split, row) scans densely): grow the lists (the
             // stream is idle here) and record them again
-            ws->lcap = (std::max<long long>(2 * ws->lcap, (long long)(1.25 * hc[4 + 5]) + 8) + 15) / 16 * 16;
+            const long long ncap =
+                (std::max<long long>(2 * ws->lcap, (long long)(1.25 * hc[4 + 5]) + 8) + 15) / 16 * 16;
+            if (lmode == 2 && list_bytes(ncap, true) > list_budget()) {
+                lmode = 0;                         // the grown lists would not fit: dense sweeps from here on
+                kavail = false;
+                continue;
+            }
+            ws->lcap = ncap;
             PINS_TRY(ensure_lists(ws, pb, st, lmode == 2));
             const int init[14] = {1, 1, -1, -1, 0, 0, hc[4 + 6], hc[4 + 7], 0, 0, 0, 0, hc[4 + 12], hc[4 + 13]};
             PINS_CUDA(cudaMemcpyAsync(ws->lctl.p, init, sizeof init, cudaMemcpyHostToDevice, st));
