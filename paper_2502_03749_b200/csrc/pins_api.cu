@@ -923,7 +923,8 @@ int sinkhorn_phase(pins_workspace *ws, const pins_problem *pb, const pins_params
         double have = 0.0;      // what the workspace already holds of these buffers is reusable
         for (int o = 0; o < 2; ++o)
             have += (double)(ws->sb[o].lj.bytes + ws->sb[o].lD.bytes + ws->sb[o].ellj.bytes + ws->sb[o].ellK.bytes);
-        return std::min(32e9, 0.5 * ((double)fr + have));
+        const double cap = getenv("PINS_LIST_BUDGET") ? atof(getenv("PINS_LIST_BUDGET")) : 32e9;   // bytes
+        return std::min(cap, 0.5 * ((double)fr + have));
     };
     auto lists_begin = [&](int mode) -> int {
         if (ws->lcap == 0) {

@@ -657,7 +657,7 @@ def test_sparse_sweeps_bit_identical(P, name, mk, monkeypatch):
 
 
 KS_KEYS = ("PINS_SPARSE_SWEEP", "PINS_LIST_CAP", "PINS_LIST_MARGIN", "PINS_KSWEEP", "PINS_KSWEEP_START",
-           "PINS_KSWEEP_NOCOOL")
+           "PINS_KSWEEP_NOCOOL", "PINS_LIST_BUDGET")
 
 
 @pytest.mark.parametrize("name,mk", [("c3s", lambda: make("c3_gmm10k", scale=0.05)),
@@ -689,6 +689,7 @@ def test_kernel_matrix_sweeps(P, name, mk, monkeypatch):
         res = []
         for env in ({"PINS_KSWEEP": "0"}, {"PINS_KSWEEP_START": "0"}, {},
                     {"PINS_KSWEEP_START": "0", "PINS_KSWEEP_NOCOOL": "1"},
+                    {"PINS_KSWEEP_START": "0", "PINS_LIST_BUDGET": "4096"},    # lists declined: dense sweeps
                     {"PINS_KSWEEP_START": "0", "PINS_LIST_CAP": "2", "PINS_LIST_MARGIN": "0.01",
                      "PINS_KSWEEP_NOCOOL": "1"}):
             for key in KS_KEYS:
@@ -709,6 +710,7 @@ def test_kernel_matrix_sweeps(P, name, mk, monkeypatch):
         scale = max(1.0, s * C.max() / w.eta)
         tol_f = 1e-13 * scale * w.eta * 41
         d = res[0]
+        assert np.array_equal(res[4][6], d[6]) and np.array_equal(res[4][7], d[7])   # declined = dense, bit for bit
         for o in res:
             assert o[0] == d[0] and o[2] == d[2], (name, k, o[:4], d[:4])
             assert abs(o[1] - d[1]) <= 1e-9 * abs(d[1]) + 1e-15
