@@ -746,6 +746,9 @@ def test_no_uninitialised_reads(P, name, scale, monkeypatch):
     # tree workspace was once reallocated at the same address and its stale factor reused.)
     w = make(name, scale=scale)
     out = []
+    # kernel-matrix sweeps from the first sweep on, so their buffers (lists, ELL tiles, unit
+    # records, packing offsets) are covered as well
+    monkeypatch.setenv("PINS_KSWEEP_START", "0")
     for z in (None, "165", "0"):
         monkeypatch.delenv("PINS_POISON", raising=False)
         if z is not None:
